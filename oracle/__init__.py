@@ -1,0 +1,210 @@
+"""ctypes wrapper of the CPU oracle (oracle/pac_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this package.  The product path
+(paper_2603_15023_b200) never imports it and shares no code with it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "pac_oracle.c")
+LIB = os.path.join(HERE, "liboracle.so")
+
+COUNT, SUM_I64, SUM_F64, AVG_F64, MIN_F64, MAX_F64 = range(6)
+M = 64
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with the host compiler (plain C, -O2, no fast-math)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-fno-fast-math",
+                               "-ffp-contract=off", "-o", LIB, SRC, "-lm"])
+    return LIB
+
+
+_lib = None
+_P = ctypes.c_void_p
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(LIB)
+        L.orc_philox4x32_10.argtypes = [_P, _P, _P]
+        L.orc_fmix64.restype = ctypes.c_uint64
+        L.orc_fmix64.argtypes = [ctypes.c_uint64]
+        L.orc_pac_hash.restype = ctypes.c_uint64
+        L.orc_pac_hash.argtypes = [ctypes.c_int64, ctypes.c_uint64]
+        L.orc_pac_hash_n.argtypes = [_P, ctypes.c_int64, ctypes.c_uint64, _P]
+        L.orc_session_init.argtypes = [ctypes.c_uint64, _P, _P, _P]
+        L.orc_pack_key.restype = ctypes.c_uint64
+        L.orc_group_keys.restype = ctypes.c_int64
+        L.orc_group_keys.argtypes = [_P, _P, ctypes.c_int, _P, ctypes.c_int64, _P, ctypes.c_int64]
+        for f in (L.orc_agg_o1, L.orc_agg_o2):
+            f.restype = ctypes.c_int
+            f.argtypes = [_P, ctypes.c_int64, _P, _P, ctypes.c_int, _P, ctypes.c_int64, _P, _P,
+                          ctypes.c_int, _P, _P, _P, _P]
+        L.orc_y_vector.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, _P, _P, _P]
+        L.orc_weighted_var.restype = ctypes.c_double
+        L.orc_weighted_var.argtypes = [_P, _P]
+        L.orc_normal.restype = ctypes.c_double
+        L.orc_normal.argtypes = [_P]
+        L.orc_posterior_update.argtypes = [_P, _P, ctypes.c_double, ctypes.c_double]
+        L.orc_finalize.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_int, _P, ctypes.c_int64,
+                                   ctypes.c_int, _P, _P, _P, _P, _P, ctypes.c_uint32, _P, _P, _P, _P]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+# ------------------------------------------------------------------ primitives
+
+def philox(ctr: Sequence[int], key: Sequence[int]) -> List[int]:
+    c = np.array(ctr, dtype=np.uint32)
+    k = np.array(key, dtype=np.uint32)
+    o = np.zeros(4, dtype=np.uint32)
+    _load().orc_philox4x32_10(_ptr(c), _ptr(k), _ptr(o))
+    return [int(v) for v in o]
+
+
+def fmix64(z: int) -> int:
+    return int(_load().orc_fmix64(z & 0xFFFFFFFFFFFFFFFF))
+
+
+def pac_hash(keys: np.ndarray, salt: int) -> np.ndarray:
+    keys = np.ascontiguousarray(keys, dtype=np.int64)
+    out = np.empty(keys.shape[0], dtype=np.uint64)
+    _load().orc_pac_hash_n(_ptr(keys), keys.shape[0], salt & 0xFFFFFFFFFFFFFFFF, _ptr(out))
+    return out
+
+
+def session(seed: int):
+    """(jstar, salt, P) for a session seed (R13)."""
+    j = ctypes.c_int(0)
+    s = ctypes.c_uint64(0)
+    P = np.zeros(M, dtype=np.float64)
+    _load().orc_session_init(seed & 0xFFFFFFFFFFFFFFFF, ctypes.byref(j), ctypes.byref(s), _ptr(P))
+    return int(j.value), int(s.value), P
+
+
+def normal_from_block(x: Sequence[int]) -> float:
+    a = np.array(x, dtype=np.uint32)
+    return float(_load().orc_normal(_ptr(a)))
+
+
+def weighted_var(P: np.ndarray, y: np.ndarray) -> float:
+    P = np.ascontiguousarray(P, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return float(_load().orc_weighted_var(_ptr(P), _ptr(y)))
+
+
+def posterior_update(P: np.ndarray, y: np.ndarray, ytilde: float, delta: float) -> np.ndarray:
+    P = np.array(P, dtype=np.float64, copy=True)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    _load().orc_posterior_update(_ptr(P), _ptr(y), float(ytilde), float(delta))
+    return P
+
+
+# ------------------------------------------------------------------ tables
+
+class _Cols:
+    def __init__(self, key_cols: Sequence[np.ndarray]):
+        self.arrs = [np.ascontiguousarray(c) for c in key_cols]
+        self.ptrs = (ctypes.c_void_p * max(1, len(self.arrs)))(*[a.ctypes.data for a in self.arrs])
+        self.eb = np.array([a.dtype.itemsize for a in self.arrs] or [0], dtype=np.int32)
+        self.n = len(self.arrs)
+
+
+def pack_keys(key_cols: Sequence[np.ndarray]) -> np.ndarray:
+    """Packed composite key per row (R20), via the oracle."""
+    cols = _Cols(key_cols)
+    n = cols.arrs[0].shape[0] if cols.n else 0
+    L = _load()
+    L.orc_pack_key.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int64]
+    return np.array([L.orc_pack_key(cols.ptrs, _ptr(cols.eb), cols.n, i) for i in range(n)],
+                    dtype=np.uint64)
+
+
+def group_keys(key_cols: Sequence[np.ndarray], masks: np.ndarray) -> np.ndarray:
+    cols = _Cols(key_cols)
+    masks = np.ascontiguousarray(masks, dtype=np.uint64)
+    n = masks.shape[0]
+    L = _load()
+    G = L.orc_group_keys(cols.ptrs, _ptr(cols.eb), cols.n, _ptr(masks), n, None, 0)
+    out = np.zeros(max(G, 1), dtype=np.uint64)
+    L.orc_group_keys(cols.ptrs, _ptr(cols.eb), cols.n, _ptr(masks), n, _ptr(out), G)
+    return out[:G]
+
+
+def agg(masks: np.ndarray, key_cols: Sequence[np.ndarray], aggs: Sequence[tuple],
+        gkeys: Optional[np.ndarray] = None, method: str = "o2") -> dict:
+    """Run O1/O2 on explicit masks.  aggs = [(kind, values or None)].
+    gkeys (sorted uint64) restricts the output to those groups (others skipped)."""
+    masks = np.ascontiguousarray(masks, dtype=np.uint64)
+    n = masks.shape[0]
+    cols = _Cols(key_cols)
+    if gkeys is None:
+        gkeys = group_keys(key_cols, masks)
+    gkeys = np.ascontiguousarray(gkeys, dtype=np.uint64)
+    G = gkeys.shape[0]
+    kinds = np.array([k for k, _ in aggs], dtype=np.int32)
+    vals = [None if v is None else np.ascontiguousarray(v) for _, v in aggs]
+    vptr = (ctypes.c_void_p * max(1, len(aggs)))(*[None if v is None else v.ctypes.data for v in vals])
+    rows = np.zeros(G, dtype=np.int64)
+    K = np.zeros(G, dtype=np.uint64)
+    count = np.zeros((G, M), dtype=np.int64)
+    worlds = []
+    for k, _ in aggs:
+        if k == COUNT:
+            worlds.append(None)
+        elif k == SUM_I64:
+            worlds.append(np.zeros((G, M), dtype=np.int64))
+        else:
+            worlds.append(np.zeros((G, M), dtype=np.float64))
+    wptr = (ctypes.c_void_p * max(1, len(aggs)))(*[None if w is None else w.ctypes.data for w in worlds])
+    fn = _load().orc_agg_o1 if method == "o1" else _load().orc_agg_o2
+    ovf = fn(_ptr(masks), n, cols.ptrs, _ptr(cols.eb), cols.n, _ptr(gkeys), G, _ptr(kinds), vptr,
+             len(aggs), _ptr(rows), _ptr(K), _ptr(count), wptr)
+    return {"G": G, "keys": gkeys, "rows": rows, "K": K, "count": count, "world": worlds,
+            "kinds": [k for k, _ in aggs], "overflow": bool(ovf)}
+
+
+def agg_from_keys(pu_keys: np.ndarray, salt: int, key_cols, aggs, gkeys=None, method="o2") -> dict:
+    return agg(pac_hash(pu_keys, salt), key_cols, aggs, gkeys=gkeys, method=method)
+
+
+def y_vector(table: dict, a: int, g: int) -> np.ndarray:
+    y = np.zeros(M, dtype=np.float64)
+    w = table["world"][a]
+    _load().orc_y_vector(table["kinds"][a], g, int(table["K"][g]), _ptr(table["count"]),
+                         _ptr(w) if w is not None else None, _ptr(y))
+    return y
+
+
+def finalize(seed: int, B: float, jstar: int, P: np.ndarray, table: dict, round_: int = 0):
+    """pac_noised over all cells of `table` (one round).  Returns
+    (release[G,A], is_null[G,A], flags[G], delta[G,A], P_after)."""
+    G = table["G"]
+    A = len(table["kinds"])
+    P = np.array(P, dtype=np.float64, copy=True)
+    kinds = np.array(table["kinds"], dtype=np.int32)
+    wptr = (ctypes.c_void_p * max(1, A))(*[None if w is None else w.ctypes.data for w in table["world"]])
+    release = np.zeros((G, A), dtype=np.float64)
+    is_null = np.zeros((G, A), dtype=np.uint8)
+    flags = np.zeros(G, dtype=np.uint8)
+    delta = np.zeros((G, A), dtype=np.float64)
+    _load().orc_finalize(seed & 0xFFFFFFFFFFFFFFFF, float(B), int(jstar), _ptr(P), G, A, _ptr(kinds),
+                         _ptr(table["K"]), _ptr(table["rows"]), _ptr(table["count"]), wptr,
+                         int(round_), _ptr(release), _ptr(is_null), _ptr(flags), _ptr(delta))
+    return release, is_null, flags, delta, P

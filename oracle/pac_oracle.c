@@ -1,0 +1,475 @@
+/*
+ * oracle/pac_oracle.c -- CPU ORACLE for the PAC stochastic-aggregation hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load, call or execute anything under
+ * oracle/.  The product path (paper_2603_15023_b200/, libpac.so) never does, and
+ * this file shares no code, header, table or constant generator with it.
+ *
+ * Plain, slow, obviously-correct C in fp64, written from PAPER.md
+ * (arxiv 2603.15023, "SIMD-PAC-DB") and the readings frozen in DESIGN.md
+ * ("Readings of the paper", R1..R19).  Every function cites the passage it follows
+ * as P:L<line> (<section>).  No blocking, fusion or reordering beyond what the
+ * definition states.
+ *
+ * Pins (tests/test_oracle_*.py, -m "not gpu"):
+ *   philox4x32_10   Random123 known-answer vectors (SC'11 generator)        pinned
+ *   fmix64          SplitMix64 reference output for seed 0                   pinned
+ *   pac_hash        popcount==32 on every key, fixed point, per-bit / pair
+ *                   statistics of a uniform balanced word; the exact flip
+ *                   selection (draw stream) has no external pin:
+ *                   "parity unpinned" beyond those properties  partial
+ *   agg_o1/agg_o2   pandas GROUP BY on each world's filtered rows (Eq. counter
+ *                   P:L249-253 / P:L956-970 as a library routine), all-ones masks
+ *                   -> plain GROUP BY, sum_j count_j == 32*rows, K == {j:count>0}  pinned
+ *   finalize        closed forms (single-PU group, y_j=j, constant y), NULL rate,
+ *                   noise std, numpy weighted variance, scipy Gaussian Bayes     pinned
+ *   posterior       scipy.stats.norm likelihood Bayes update                    pinned
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_M 64 /* m = 64 worlds, P:L92 (§2) */
+
+/* ------------------------------------------------------------------ Philox4x32-10
+ * DESIGN.md R13 (the paper is silent on the RNG).  Salmon, Moraes, Dror, Shaw,
+ * "Parallel random numbers: as easy as 1, 2, 3" (SC'11): round function
+ *   (c0,c1,c2,c3) -> (hi(M1*c2)^c1^k0, lo(M1*c2), hi(M0*c0)^c3^k1, lo(M0*c0)),
+ * key bumped by the Weyl constants between rounds, 10 rounds. */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; r++) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+    uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    uint32_t n1 = (uint32_t)p1;
+    uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    uint32_t n3 = (uint32_t)p0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Philox block for (seed, counter words).  seed is the 64-bit session seed (key). */
+static void philox_block(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                         uint32_t out[4]) {
+  uint32_t ctr[4] = {c0, c1, c2, c3};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  orc_philox4x32_10(ctr, key, out);
+}
+
+enum { TAG_CELL = 0, TAG_JSTAR = 1, TAG_SALT = 2 }; /* DESIGN.md R13 */
+
+/* ------------------------------------------------------------------ fmix64
+ * DESIGN.md R1: the base hash the paper wraps ("We wrap DuckDB's hash function",
+ * P:L93 §2) is read as the SplitMix64 finalizer (Stafford Mix13 constants). */
+uint64_t orc_fmix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+static int popcount64(uint64_t x) {
+  int c = 0;
+  for (int j = 0; j < 64; j++) c += (int)((x >> j) & 1u);
+  return c;
+}
+
+/* ------------------------------------------------------------------ pac_hash
+ * P:L93 (§2): pac_hash re-hashes per query with a salt and "cheaply transform[s]
+ * the binomially distributed hash number in a random hash that is guaranteed to
+ * have 32 0- and 32 1-bits"; P:L949-952 (§4): keyed hash, per-query key K;
+ * `\iffalse` P:L1651: effective hash pac_hash(h(u) XOR q).
+ * DESIGN.md R1 (mix) + R2 (balancing, "rejection flips"):
+ *   x = fmix64(key XOR salt); c = popcount(x); if c == 32 -> x.
+ *   maj = (c > 32); k = |c - 32|.
+ *   w_0 = fmix64(x XOR 0xD1B54A32D192ED03); w_{i+1} = fmix64(w_i + 0x9E3779B97F4A7C15).
+ *   Each word gives 10 draws p = (w >> 6t) & 63, t = 0..9 (top 4 bits unused).
+ *   For each draw: if bit p of the current x equals maj, flip it and k--; stop at k = 0.
+ *   Safety net (never reached in practice): after 64 words, flip the remaining k
+ *   majority bits from the lowest position upward. */
+uint64_t orc_pac_hash(int64_t key, uint64_t salt) {
+  uint64_t x = orc_fmix64((uint64_t)key ^ salt);
+  int c = popcount64(x);
+  if (c == 32) return x;
+  uint64_t maj = (c > 32) ? 1u : 0u;
+  int k = (c > 32) ? (c - 32) : (32 - c);
+  uint64_t w = orc_fmix64(x ^ 0xD1B54A32D192ED03ull);
+  for (int word = 0; word < 64; word++) {
+    for (int t = 0; t < 10; t++) {
+      int p = (int)((w >> (6 * t)) & 63u);
+      if (((x >> p) & 1u) == maj) {
+        x ^= (1ull << p);
+        k--;
+        if (k == 0) return x;
+      }
+    }
+    w = orc_fmix64(w + 0x9E3779B97F4A7C15ull);
+  }
+  for (int p = 0; p < 64 && k > 0; p++) {
+    if (((x >> p) & 1u) == maj) {
+      x ^= (1ull << p);
+      k--;
+    }
+  }
+  return x;
+}
+
+void orc_pac_hash_n(const int64_t* keys, int64_t n, uint64_t salt, uint64_t* out) {
+  for (int64_t i = 0; i < n; i++) out[i] = orc_pac_hash(keys[i], salt);
+}
+
+/* ------------------------------------------------------------------ session
+ * P:L886 (§4): "sample a secret world index uniformly at random j* <- {1..m},
+ * initialize ... P = (1/m, ..., 1/m)"; P:L99 (§2): one j* per query shared by all
+ * cells; P:L93 / P:L950: a fresh per-query hash key (salt).
+ * DESIGN.md R13: j* = x0 & 63 of Philox(seed; 0,0,0,TAG_JSTAR);
+ *                salt = x0 | x1<<32 of Philox(seed; 0,0,0,TAG_SALT). */
+void orc_session_init(uint64_t seed, int* jstar, uint64_t* salt, double* P) {
+  uint32_t o[4];
+  philox_block(seed, 0, 0, 0, TAG_JSTAR, o);
+  *jstar = (int)(o[0] & 63u);
+  philox_block(seed, 0, 0, 0, TAG_SALT, o);
+  *salt = (uint64_t)o[0] | ((uint64_t)o[1] << 32);
+  for (int j = 0; j < ORC_M; j++) P[j] = 1.0 / ORC_M;
+}
+
+/* ------------------------------------------------------------------ group keys
+ * DESIGN.md R20: composite group key = concatenation (first column most
+ * significant) of each column's bits with the sign bit flipped, so unsigned order
+ * of the packed key == lexicographic order of the signed column values. */
+uint64_t orc_pack_key(const void* const* cols, const int32_t* elem_bytes, int n_keys, int64_t row) {
+  uint64_t packed = 0;
+  for (int c = 0; c < n_keys; c++) {
+    int w = elem_bytes[c];
+    uint64_t v;
+    if (w == 1) v = (uint64_t)(uint8_t)((const int8_t*)cols[c])[row];
+    else if (w == 2) v = (uint64_t)(uint16_t)((const int16_t*)cols[c])[row];
+    else if (w == 4) v = (uint64_t)(uint32_t)((const int32_t*)cols[c])[row];
+    else v = (uint64_t)((const int64_t*)cols[c])[row];
+    v ^= 1ull << (8 * w - 1);
+    packed = (w == 8) ? v : ((packed << (8 * w)) | v);
+  }
+  return packed;
+}
+
+static int cmp_u64(const void* a, const void* b) {
+  uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return (x > y) - (x < y);
+}
+
+/* Distinct packed keys (ascending) of rows with a nonzero mask.  DESIGN.md R21:
+ * rows whose world mask is 0 belong to no world ("we filter out rows where
+ * this updated pu=0") and create no group.  With n_keys == 0 (ungrouped) there is
+ * always exactly one group, key 0 (SQL: an ungrouped aggregate returns one row).
+ * Returns G; writes min(G, cap) keys. */
+int64_t orc_group_keys(const void* const* cols, const int32_t* elem_bytes, int n_keys,
+                       const uint64_t* masks, int64_t n, uint64_t* out, int64_t cap) {
+  if (n_keys == 0) {
+    if (cap > 0) out[0] = 0;
+    return 1;
+  }
+  uint64_t* tmp = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(n > 0 ? n : 1));
+  int64_t m = 0;
+  for (int64_t i = 0; i < n; i++)
+    if (masks[i] != 0) tmp[m++] = orc_pack_key(cols, elem_bytes, n_keys, i);
+  qsort(tmp, (size_t)m, sizeof(uint64_t), cmp_u64);
+  int64_t g = 0;
+  for (int64_t i = 0; i < m; i++) {
+    if (i == 0 || tmp[i] != tmp[i - 1]) {
+      if (g < cap) out[g] = tmp[i];
+      g++;
+    }
+  }
+  free(tmp);
+  return g;
+}
+
+static int64_t find_group(const uint64_t* gkeys, int64_t G, uint64_t key) {
+  int64_t lo = 0, hi = G;
+  while (lo < hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (gkeys[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return (lo < G && gkeys[lo] == key) ? lo : -1;
+}
+
+/* ------------------------------------------------------------------ aggregation
+ * Aggregate kinds (agg in {sum, count, avg, min, max}). */
+enum { K_COUNT = 0, K_SUM_I64 = 1, K_SUM_F64 = 2, K_AVG_F64 = 3, K_MIN_F64 = 4, K_MAX_F64 = 5 };
+
+/* Neumaier-compensated running sum (oracle-side accuracy only; the definition is
+ * the exact sum). */
+typedef struct { double s, c; } csum;
+static void csum_add(csum* a, double v) {
+  double t = a->s + v;
+  if (fabs(a->s) >= fabs(v)) a->c += (a->s - t) + v; else a->c += (v - t) + a->s;
+  a->s = t;
+}
+
+/* Output table, canonical group order (ascending packed key = gkeys):
+ *   rows[G]              rows with nonzero mask in the group (int64)
+ *   K[G]                 OR of the row masks ("K <- K | h")
+ *   count[G*64]          per-world row count (int64), P:L87 / P:L2255
+ *   world[a][G*64]       per aggregate a: int64 (SUM_I64) or double (others);
+ *                        SUM_F64/AVG_F64 hold the world's value sum (AVG divides at
+ *                        finalize, R6); MIN/MAX hold the extreme, +inf / -inf when
+ *                        the world is empty.
+ * Returns 0, or 1 if some int64 world sum overflowed (checked with __int128, R15). */
+static void init_world(int kind, void* w, int64_t G) {
+  for (int64_t i = 0; i < G * ORC_M; i++) {
+    if (kind == K_SUM_I64) ((int64_t*)w)[i] = 0;
+    else if (kind == K_MIN_F64) ((double*)w)[i] = INFINITY;
+    else if (kind == K_MAX_F64) ((double*)w)[i] = -INFINITY;
+    else if (kind != K_COUNT) ((double*)w)[i] = 0.0;
+  }
+}
+
+/* O2: single pass.  For every row, for j = 0..63, update world j iff bit j of the
+ * row's mask is set -- PacCountUpdate P:L2254-2258 (read with ">> j", R4)
+ * generalised to SUM/AVG/MIN/MAX per §5 P:L1737 ("the value at position j
+ * accumulates contributions from those rows whose key_hash has bit j set"). */
+int orc_agg_o2(const uint64_t* masks, int64_t n, const void* const* cols, const int32_t* elem_bytes,
+               int n_keys, const uint64_t* gkeys, int64_t G, const int32_t* kinds,
+               const void* const* values, int n_aggs, int64_t* rows, uint64_t* K, int64_t* count,
+               void* const* world) {
+  int overflow = 0;
+  for (int64_t g = 0; g < G; g++) { rows[g] = 0; K[g] = 0; }
+  for (int64_t i = 0; i < G * ORC_M; i++) count[i] = 0;
+  for (int a = 0; a < n_aggs; a++) if (world[a]) init_world(kinds[a], world[a], G);
+  __int128* isum = (__int128*)calloc((size_t)(G * ORC_M * n_aggs + 1), sizeof(__int128));
+  csum* fsum = (csum*)calloc((size_t)(G * ORC_M * n_aggs + 1), sizeof(csum));
+  for (int64_t r = 0; r < n; r++) {
+    uint64_t h = masks[r];
+    if (h == 0) continue;
+    uint64_t key = n_keys ? orc_pack_key(cols, elem_bytes, n_keys, r) : 0;
+    int64_t g = find_group(gkeys, G, key);
+    if (g < 0) continue;
+    rows[g] += 1;
+    K[g] |= h;
+    for (int j = 0; j < ORC_M; j++) {
+      if (((h >> j) & 1u) == 0) continue;
+      int64_t cell = g * ORC_M + j;
+      count[cell] += 1;
+      for (int a = 0; a < n_aggs; a++) {
+        int64_t idx = ((int64_t)a * G) * ORC_M + cell;
+        switch (kinds[a]) {
+          case K_SUM_I64: isum[idx] += (__int128)((const int64_t*)values[a])[r]; break;
+          case K_SUM_F64:
+          case K_AVG_F64: csum_add(&fsum[idx], ((const double*)values[a])[r]); break;
+          case K_MIN_F64: {
+            double v = ((const double*)values[a])[r];
+            double* e = &((double*)world[a])[cell];
+            if (v < *e) *e = v;
+            break;
+          }
+          case K_MAX_F64: {
+            double v = ((const double*)values[a])[r];
+            double* e = &((double*)world[a])[cell];
+            if (v > *e) *e = v;
+            break;
+          }
+          default: break;
+        }
+      }
+    }
+  }
+  for (int a = 0; a < n_aggs; a++) {
+    for (int64_t cell = 0; cell < G * ORC_M; cell++) {
+      int64_t idx = ((int64_t)a * G) * ORC_M + cell;
+      if (kinds[a] == K_SUM_I64) {
+        __int128 s = isum[idx];
+        if (s > (__int128)INT64_MAX || s < (__int128)INT64_MIN) overflow = 1;
+        ((int64_t*)world[a])[cell] = (int64_t)s;
+      } else if (kinds[a] == K_SUM_F64 || kinds[a] == K_AVG_F64) {
+        ((double*)world[a])[cell] = fsum[idx].s + fsum[idx].c;
+      }
+    }
+  }
+  free(isum);
+  free(fsum);
+  return overflow;
+}
+
+/* O1: the PAC-DB m-fold semantics with hash-coupled worlds (§4, coupled
+ * per P:L1028-1030): for each world j, the sampled instance I^(j) is the rows whose
+ * mask has bit j set; run the plain GROUP BY on it; then List the 64
+ * per-world results per group.  Groups absent from world j keep count 0
+ * and the empty-aggregate sentinels (NULL mechanism P:L1654, R9). */
+int orc_agg_o1(const uint64_t* masks, int64_t n, const void* const* cols, const int32_t* elem_bytes,
+               int n_keys, const uint64_t* gkeys, int64_t G, const int32_t* kinds,
+               const void* const* values, int n_aggs, int64_t* rows, uint64_t* K, int64_t* count,
+               void* const* world) {
+  int overflow = 0;
+  int64_t* gid = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  for (int64_t r = 0; r < n; r++) {
+    uint64_t key = n_keys ? orc_pack_key(cols, elem_bytes, n_keys, r) : 0;
+    gid[r] = masks[r] ? find_group(gkeys, G, key) : -1;
+  }
+  for (int64_t g = 0; g < G; g++) { rows[g] = 0; K[g] = 0; }
+  for (int64_t r = 0; r < n; r++)
+    if (gid[r] >= 0) { rows[gid[r]] += 1; K[gid[r]] |= masks[r]; }
+  for (int a = 0; a < n_aggs; a++) if (world[a]) init_world(kinds[a], world[a], G);
+  /* per-world plain GROUP BY state */
+  int64_t* cnt = (int64_t*)malloc(sizeof(int64_t) * (size_t)(G + 1));
+  __int128* is = (__int128*)malloc(sizeof(__int128) * (size_t)(G + 1));
+  csum* fs = (csum*)malloc(sizeof(csum) * (size_t)(G + 1));
+  double* ex = (double*)malloc(sizeof(double) * (size_t)(G + 1));
+  for (int j = 0; j < ORC_M; j++) {
+    /* COUNT(*) over I^(j) */
+    for (int64_t g = 0; g < G; g++) cnt[g] = 0;
+    for (int64_t r = 0; r < n; r++)
+      if (gid[r] >= 0 && ((masks[r] >> j) & 1u)) cnt[gid[r]] += 1;
+    for (int64_t g = 0; g < G; g++) count[g * ORC_M + j] = cnt[g];
+    for (int a = 0; a < n_aggs; a++) {
+      int kind = kinds[a];
+      if (kind == K_COUNT) continue;
+      for (int64_t g = 0; g < G; g++) {
+        is[g] = 0; fs[g].s = 0; fs[g].c = 0;
+        ex[g] = (kind == K_MIN_F64) ? INFINITY : -INFINITY;
+      }
+      for (int64_t r = 0; r < n; r++) {
+        if (gid[r] < 0 || !((masks[r] >> j) & 1u)) continue;
+        int64_t g = gid[r];
+        if (kind == K_SUM_I64) is[g] += (__int128)((const int64_t*)values[a])[r];
+        else if (kind == K_SUM_F64 || kind == K_AVG_F64) csum_add(&fs[g], ((const double*)values[a])[r]);
+        else if (kind == K_MIN_F64) { double v = ((const double*)values[a])[r]; if (v < ex[g]) ex[g] = v; }
+        else if (kind == K_MAX_F64) { double v = ((const double*)values[a])[r]; if (v > ex[g]) ex[g] = v; }
+      }
+      for (int64_t g = 0; g < G; g++) {
+        int64_t cell = g * ORC_M + j;
+        if (kind == K_SUM_I64) {
+          if (is[g] > (__int128)INT64_MAX || is[g] < (__int128)INT64_MIN) overflow = 1;
+          ((int64_t*)world[a])[cell] = (int64_t)is[g];
+        } else if (kind == K_SUM_F64 || kind == K_AVG_F64) {
+          ((double*)world[a])[cell] = fs[g].s + fs[g].c;
+        } else {
+          ((double*)world[a])[cell] = ex[g];
+        }
+      }
+    }
+  }
+  free(gid); free(cnt); free(is); free(fs); free(ex);
+  return overflow;
+}
+
+/* ------------------------------------------------------------------ finalize
+ * The fused pac_noised step (§2; final mechanism P:L841-850 §4).
+ *
+ * y-vector (R7, R9): for a world j whose K bit is set, COUNT -> 2*count_j,
+ * SUM -> 2*sum_j ("count[j*]*2 + noise", "2*(C_pos - C_neg)"),
+ * AVG -> fsum_j / count_j (per-world divisor, R6), MIN/MAX -> ext_j; a world whose
+ * K bit is unset reads as 0 ("counters corresponding to unset bits are
+ * treated as zeros").
+ */
+void orc_y_vector(int kind, int64_t g, uint64_t Kg, const int64_t* count, const void* world,
+                  double y[64]) {
+  for (int j = 0; j < ORC_M; j++) {
+    int64_t cell = g * ORC_M + j;
+    if (((Kg >> j) & 1u) == 0) { y[j] = 0.0; continue; }
+    switch (kind) {
+      case K_COUNT: y[j] = 2.0 * (double)count[cell]; break;
+      case K_SUM_I64: y[j] = 2.0 * (double)((const int64_t*)world)[cell]; break;
+      case K_SUM_F64: y[j] = 2.0 * ((const double*)world)[cell]; break;
+      case K_AVG_F64: y[j] = ((const double*)world)[cell] / (double)count[cell]; break;
+      default: y[j] = ((const double*)world)[cell]; break;
+    }
+  }
+}
+
+/* Var_{j~P}[y_j] (R8): population variance weighted by P, two-pass,
+ * j ascending.  R11: exactly 0 when every y_j with P_j > 0 is equal. */
+double orc_weighted_var(const double P[64], const double y[64]) {
+  int first = -1, all_equal = 1;
+  for (int j = 0; j < ORC_M; j++) {
+    if (P[j] > 0.0) {
+      if (first < 0) first = j;
+      else if (y[j] != y[first]) all_equal = 0;
+    }
+  }
+  if (all_equal) return 0.0;
+  double mu = 0.0;
+  for (int j = 0; j < ORC_M; j++) mu += P[j] * y[j];
+  double s2 = 0.0;
+  for (int j = 0; j < ORC_M; j++) s2 += P[j] * (y[j] - mu) * (y[j] - mu);
+  return s2;
+}
+
+/* Standard normal from one Philox block (R13, Box-Muller):
+ *   u1 = (((x1 << 21) ^ (x2 >> 11)) + 0.5) * 2^-53,  u2 = (x3 + 0.5) * 2^-32,
+ *   z  = sqrt(-2 ln u1) * cos(2 pi u2). */
+double orc_normal(const uint32_t x[4]) {
+  uint64_t m53 = ((uint64_t)x[1] << 21) ^ (uint64_t)(x[2] >> 11);
+  double u1 = ((double)m53 + 0.5) * 0x1.0p-53;
+  double u2 = ((double)x[3] + 0.5) * 0x1.0p-32;
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
+}
+
+/* Bayesian posterior update (§4; §2):
+ *   P <- (P .* W) / sum(P .* W),  W_j = exp(-(y~ - y_j)^2 / (2 Delta)).
+ * R14: over worlds with P_j > 0, W_j = exp(-(d_j - min_i d_i) / (2 Delta)) with
+ * d_j = (y~ - y_j)^2 -- identical after normalisation, and never all zero. */
+void orc_posterior_update(double P[64], const double y[64], double ytilde, double delta) {
+  double d[64], dmin = INFINITY;
+  for (int j = 0; j < ORC_M; j++) {
+    d[j] = (ytilde - y[j]) * (ytilde - y[j]);
+    if (P[j] > 0.0 && d[j] < dmin) dmin = d[j];
+  }
+  double tot = 0.0;
+  for (int j = 0; j < ORC_M; j++) {
+    if (P[j] > 0.0) P[j] = P[j] * exp(-(d[j] - dmin) / (2.0 * delta));
+    tot += P[j];
+  }
+  for (int j = 0; j < ORC_M; j++) P[j] = P[j] / tot;
+}
+
+/* pac_noised over every cell of a table, canonical order (R12: groups ascending,
+ * aggregates in declared order; one call = one round).  Per cell:
+ *   x = Philox(seed; cell_lo, cell_hi, round, TAG_CELL), cell = g*A + a
+ *   NULL iff (x0 >> 26) >= popcount(K_g)        (R10)
+ *   s2 = Var_P[y]; Delta = s2 / (2B)
+ *   s2 == 0 -> release y_{j*}, no update         (R11)
+ *   else release y_{j*} + sqrt(Delta) * z, then posterior update
+ * flags[g] bit 0: diversity check (R18): rows >= 64 and
+ * popcount(K) <= 34. */
+void orc_finalize(uint64_t seed, double B, int jstar, double P[64], int64_t G, int n_aggs,
+                  const int32_t* kinds, const uint64_t* K, const int64_t* rows, const int64_t* count,
+                  const void* const* world, uint32_t round, double* release, uint8_t* is_null,
+                  uint8_t* flags, double* delta_out) {
+  double y[64];
+  for (int64_t g = 0; g < G; g++) {
+    int pc = popcount64(K[g]);
+    if (flags) flags[g] = (uint8_t)((rows[g] >= 64 && pc <= 34) ? 1 : 0);
+    for (int a = 0; a < n_aggs; a++) {
+      int64_t cell = g * n_aggs + a;
+      uint32_t x[4];
+      philox_block(seed, (uint32_t)cell, (uint32_t)((uint64_t)cell >> 32), round, TAG_CELL, x);
+      if ((int)(x[0] >> 26) >= pc) {
+        is_null[cell] = 1;
+        release[cell] = NAN;
+        if (delta_out) delta_out[cell] = NAN;
+        continue;
+      }
+      is_null[cell] = 0;
+      orc_y_vector(kinds[a], g, K[g], count, world[a], y);
+      double s2 = orc_weighted_var(P, y);
+      double delta = s2 / (2.0 * B);
+      if (delta_out) delta_out[cell] = delta;
+      if (s2 == 0.0) {
+        release[cell] = y[jstar];
+        continue;
+      }
+      double yt = y[jstar] + sqrt(delta) * orc_normal(x);
+      release[cell] = yt;
+      orc_posterior_update(P, y, yt, delta);
+    }
+  }
+}
