@@ -1,0 +1,62 @@
+"""Builds every native artefact in-tree (they travel to the GPU box with gpurun):
+
+  paper_2603_15023_b200/libpac.so   libpac, sm_100a (the product)
+  datagen/libdatagen.so             device-side synthetic input generator
+  oracle/liboracle.so               CPU oracle (plain C, host compiler; test infrastructure)
+
+Usage: python build.py [--force] [--verbose]
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+           "-Xptxas", "-v"]
+
+TARGETS = {
+    "libpac": (os.path.join(ROOT, "paper_2603_15023_b200", "libpac.so"),
+               sorted(glob.glob(os.path.join(ROOT, "paper_2603_15023_b200", "csrc", "*.cu"))),
+               glob.glob(os.path.join(ROOT, "paper_2603_15023_b200", "csrc", "*.cuh"))
+               + [os.path.join(ROOT, "include", "pac.h")]),
+    "datagen": (os.path.join(ROOT, "datagen", "libdatagen.so"),
+                [os.path.join(ROOT, "datagen", "csrc", "datagen.cu")], []),
+}
+
+
+def _stale(out, deps):
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_cuda(name: str, force: bool = False, verbose: bool = False) -> str:
+    out, srcs, hdrs = TARGETS[name]
+    if force or _stale(out, srcs + hdrs):
+        cmd = [NVCC] + ARCH + NVFLAGS + ["-I", os.path.join(ROOT, "include"), "-o", out] + srcs
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed for {name}")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    return out
+
+
+def build_all(force: bool = False, verbose: bool = False):
+    sys.path.insert(0, ROOT)
+    out = [build_cuda("libpac", force, verbose), build_cuda("datagen", force, verbose)]
+    import oracle
+    out.append(oracle.build(force))
+    return out
+
+
+if __name__ == "__main__":
+    for p in build_all(force="--force" in sys.argv, verbose="--verbose" in sys.argv):
+        print(p)

@@ -1,0 +1,216 @@
+/*
+ * pac.h -- C-ABI of libpac.so: the B200-native (sm_100a) hot path of
+ * "SIMD-PAC-DB: Pretty Performant PAC Privacy" (arXiv 2603.15023).
+ *
+ * One data-parallel path: per-row privacy-unit (PU) key -> 64-bit world mask with
+ * exactly 32 bits set (pac_hash, §2, §4); single-pass
+ * accumulation of COUNT/SUM/AVG/MIN/MAX for all m = 64 possible worlds per group
+ * (pac_agg, Eq. counter, §4; §5); and the
+ * noised release pac_noised with the Bayesian posterior update (§4).
+ * Readings of ambiguous passages are DESIGN.md R1..R21; the same readings are
+ * implemented, independently, by the CPU oracle under oracle/.
+ *
+ * Conventions (every entry point):
+ *  - d_* pointers are DEVICE pointers owned by the caller (e.g. PyTorch tensors);
+ *    h_* pointers are host pointers owned by the caller.  The library owns only
+ *    pac_session objects (opaque) and never frees caller memory.
+ *  - Calls are asynchronous on `stream` unless documented as synchronizing; the
+ *    caller keeps every buffer alive until the stream has passed the call.
+ *  - Return value: PAC_OK or a negative-free status code below; no exception or
+ *    longjmp crosses the ABI.  Device-side conditions that can only be known after
+ *    the kernels ran (group capacity, int64 overflow) are reported in the table's
+ *    d_status word (see pac_table) and by pac_table_check().
+ *  - Layouts are row-major.  "[G][64]" means 64 consecutive elements per group,
+ *    element j = world j (world j <-> bit j of the mask, LSB = world 0, R3).
+ */
+#ifndef PAC_H_
+#define PAC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PAC_M 64         /* worlds per PU hash, P:L92 (§2) */
+#define PAC_MAX_AGGS 8   /* aggregates per pac_agg_grouped call */
+#define PAC_MAX_KEYS 4   /* group-by key columns, total width <= 8 bytes (R20) */
+
+typedef struct CUstream_st* pac_stream_t; /* a cudaStream_t; NULL = legacy default stream */
+
+enum {
+  PAC_OK = 0,
+  PAC_E_INVAL = 1,      /* bad argument: NULL/size mismatch, both or neither mask source,
+                           unsupported aggregate combination, unaligned column */
+  PAC_E_CAPACITY = 2,   /* more distinct groups than G_cap (pac_table_check) */
+  PAC_E_WORKSPACE = 3,  /* ws_bytes smaller than the *_workspace_size() answer */
+  PAC_E_CUDA = 4,       /* a CUDA runtime call or kernel launch failed */
+  PAC_E_OVERFLOW = 5    /* an int64 world sum overflowed (R15 precondition violated) */
+};
+
+/* Aggregate kinds (agg in {sum, count, avg, min, max}).  Values: SUM_I64 reads
+ * an int64 column, the f64 kinds a double column, COUNT none. */
+typedef enum {
+  PAC_COUNT = 0,
+  PAC_SUM_I64 = 1,
+  PAC_SUM_F64 = 2,
+  PAC_AVG_F64 = 3,
+  PAC_MIN_F64 = 4,
+  PAC_MAX_F64 = 5
+} pac_agg_kind;
+
+typedef struct {
+  int32_t kind;          /* pac_agg_kind */
+  const void* d_values;  /* [n_rows] int64 or double; NULL for PAC_COUNT */
+} pac_agg_spec;
+
+typedef struct {
+  const void* d_col;     /* [n_rows] signed integer key column */
+  int32_t elem_bytes;    /* 1, 2, 4 or 8 */
+} pac_key_col;
+
+/* ------------------------------------------------------------------ session (§8 a1)
+ * P:L886 (§4): "sample a secret world index uniformly at random j* ..., initialize ...
+ * P = (1/m, ..., 1/m)"; P:L99 (§2): one j* per query shared by all cells; P:L93 /
+ * a fresh per-query hash key.  R13: j* = x0 & 63 of Philox4x32-10(seed;
+ * 0,0,0,1), salt = x0 | x1<<32 of Philox(seed; 0,0,0,2).  budget_B is the per-release
+ * MI budget B (BASELINE uses 1/128).  The session owns a device copy of P and is
+ * single-owner and strictly sequential (noising order matters). */
+typedef struct pac_session pac_session;
+
+/* Creates a session on the current CUDA device.  Errors: PAC_E_INVAL (out NULL,
+ * budget_B <= 0 or not finite), PAC_E_CUDA. */
+int pac_session_create(uint64_t seed, double budget_B, pac_session** out);
+/* Frees the session (synchronizes the device).  NULL is a no-op. */
+int pac_session_destroy(pac_session* s);
+/* Synchronizing read of the session state.  Any output pointer may be NULL.
+ * h_P64: 64 doubles.  releases: number of non-NULL, non-zero-variance releases so far. */
+int pac_session_query(const pac_session* s, uint64_t* salt, int32_t* jstar, double* h_P64,
+                      uint64_t* releases, uint64_t* seed, double* budget_B);
+/* Overwrites the posterior with 64 host doubles (resume / tests).  Synchronizing. */
+int pac_session_set_posterior(pac_session* s, const double* h_P64);
+/* Device pointer of the session's posterior P[64] (owned by the session). */
+double* pac_session_posterior_device(pac_session* s);
+
+/* ------------------------------------------------------------------ mask (§8 a2)
+ * pac_hash (§2; §4; effective hash pac_hash(h(u) XOR q)):
+ *   d_mask[i] = balance(fmix64(uint64(d_pu_key[i]) XOR salt))     (R1, R2)
+ * popcount(d_mask[i]) == 32 for every i.  n may be 0.  Errors: PAC_E_INVAL (n < 0,
+ * NULL pointer with n > 0), PAC_E_CUDA. */
+int pac_mask(const int64_t* d_pu_key, int64_t n, uint64_t salt, uint64_t* d_mask,
+             pac_stream_t stream);
+
+/* ------------------------------------------------------------------ aggregation (§8 a3-a5)
+ * Output table in canonical order: groups ascending by packed key (R20).  Capacity
+ * G_cap groups; all arrays caller-allocated with that capacity.
+ *
+ *   d_num_groups [1]        int64  number of distinct groups (may exceed G_cap: then
+ *                                  the table is invalid and d_status has CAPACITY)
+ *   d_status     [1]        int32  0 or PAC_E_CAPACITY / PAC_E_OVERFLOW
+ *   d_group_key  [G_cap]    uint64 packed composite key (R20); 0 when ungrouped
+ *   d_rows       [G_cap]    int64  rows with a nonzero mask in the group (R21)
+ *   d_presence   [G_cap]    uint64 K = OR of the group's masks (R5)
+ *   d_count      [G_cap][64] int64 per-world row count.  REQUIRED unless every
+ *                                  aggregate is MIN/MAX (then NULL)
+ *   d_world[a]   [G_cap][64]       per aggregate a: int64 for SUM_I64; double for
+ *                                  SUM_F64 / AVG_F64 (the world's value SUM -- AVG
+ *                                  divides by d_count at finalize, R6) and MIN/MAX
+ *                                  (+inf / -inf for a world with no row); NULL for COUNT
+ */
+typedef struct {
+  int64_t* d_num_groups;
+  int32_t* d_status;
+  uint64_t* d_group_key;
+  int64_t* d_rows;
+  uint64_t* d_presence;
+  int64_t* d_count;
+  void* d_world[PAC_MAX_AGGS];
+} pac_table;
+
+/* Workspace bytes for pac_agg_grouped with these aggregates and capacity. */
+int pac_agg_workspace_size(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, size_t* bytes);
+
+/* Single-pass 64-world grouped aggregation (§5; PacCountUpdate P:L2254-2258
+ * read with ">> j", R4).  For every row r with mask h_r != 0 in group g, and every
+ * world j with bit j of h_r set:
+ *   count[g][j] += 1; SUM: world[a][g][j] += v_r; AVG: world[a][g][j] += v_r;
+ *   MIN/MAX: world[a][g][j] = min/max(world[a][g][j], v_r); rows[g] += 1; K[g] |= h_r.
+ * Masks: exactly one of d_pu_key (hashed in-kernel with `salt`, = pac_mask) and d_mask
+ * (explicit masks, e.g. pac_select-ed ones) is non-NULL.
+ * keys: n_keys in 0..PAC_MAX_KEYS columns (n_keys = 0: one group, R21).
+ * Limits: n_aggs <= PAC_MAX_AGGS; at most 2 distinct int64 SUM columns, 2 distinct f64
+ * SUM/AVG columns and 1 f64 MIN/MAX column per call (else PAC_E_INVAL).
+ * MIN/MAX-only calls take the pruned path: a row that cannot improve a
+ * group's bound min_j MAX_j (resp. max_j MIN_j) is skipped without hashing.
+ * Integer results are exact and order-independent; f64 sums are order-dependent in the
+ * last bits (<= 1e-9 relative to the exact sum, R16).
+ * Errors (synchronous): PAC_E_INVAL, PAC_E_WORKSPACE, PAC_E_CUDA.
+ * Errors (asynchronous, in *d_status): PAC_E_CAPACITY, PAC_E_OVERFLOW. */
+int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, uint64_t salt,
+                    const pac_key_col* keys, int n_keys, const pac_agg_spec* aggs, int n_aggs,
+                    int64_t n_rows, const pac_table* out, int64_t G_cap, void* d_ws,
+                    size_t ws_bytes, pac_stream_t stream);
+
+/* Synchronizing check of a table: *h_num_groups and the status code (PAC_OK,
+ * PAC_E_CAPACITY, PAC_E_OVERFLOW). */
+int pac_table_check(const pac_table* t, int64_t* h_num_groups, pac_stream_t stream);
+
+/* Re-derives K after a cross-GPU merge (NCCL has no bitwise-OR reduction, §8e):
+ * K[g] bit j = (count[g][j] > 0) when d_count is present, else (the MIN or MAX world
+ * value is not its empty sentinel).  Uses the device-side num_groups. */
+int pac_table_rederive_presence(const pac_table* t, const pac_agg_spec* aggs, int n_aggs,
+                                int64_t G_cap, pac_stream_t stream);
+
+/* Scatters table `in` (G_in groups, keys a subset of d_union_keys) into table `out`
+ * laid out by the ascending union dictionary d_union_keys[G_union]; groups absent from
+ * `in` get the empty state (count 0, sums 0, MIN +inf, MAX -inf, rows 0, K 0).  Used so
+ * that all ranks share one layout before the allreduce.  `in`'s num_groups is read
+ * from the device. */
+int pac_table_remap(const pac_table* in, const uint64_t* d_union_keys, int64_t G_union,
+                    const pac_agg_spec* aggs, int n_aggs, int64_t G_cap_in,
+                    const pac_table* out, pac_stream_t stream);
+
+/* ------------------------------------------------------------------ finalize (§8 a6-a7)
+ * The fused pac_noised step (§2; §4) over every cell of a table,
+ * cells in canonical order g*n_aggs + a (R12); one call = one round `round`.
+ * Per cell (Philox4x32-10 key = session seed, counter = (cell_lo, cell_hi, round, 0)):
+ *   NULL iff (x0 >> 26) >= popcount(K[g])                              (R10)
+ *   y_j = 2*count_j | 2*sum_j | fsum_j/count_j | ext_j for K bit j set, else 0 (R7, R9)
+ *   s2 = Var_{j~P}[y]; Delta = s2/(2B)                                  (R8)
+ *   s2 == 0 (all y_j with P_j > 0 equal): release y_{j*}, no update     (R11)
+ *   else release = y_{j*} + sqrt(Delta)*z, z Box-Muller of (x1,x2,x3)   (R13)
+ *        P <- P*W/sum(P*W), W_j = exp(-(d_j - min d)/(2 Delta))         (R14)
+ * Outputs (caller-allocated, [G_cap][n_aggs] unless noted):
+ *   d_release (NaN for NULL cells), d_is_null (0/1), d_flags [G_cap] bit 0 = diversity
+ *   check (rows >= 64 and popcount K <= 34, R18), d_delta (optional, may
+ *   be NULL; NaN for NULL cells).
+ * The session posterior is updated in place on the device, in cell order.
+ * Errors: PAC_E_INVAL, PAC_E_WORKSPACE, PAC_E_CUDA. */
+int pac_finalize_workspace_size(int64_t G_cap, int n_aggs, size_t* bytes);
+int pac_finalize(pac_session* s, const pac_table* t, const pac_agg_spec* aggs, int n_aggs,
+                 int64_t G_cap, uint32_t round, double* d_release, uint8_t* d_is_null,
+                 uint8_t* d_flags, double* d_delta, void* d_ws, size_t ws_bytes,
+                 pac_stream_t stream);
+
+/* Standalone Bayesian posterior update: with y = d_y64[64] (device),
+ *   P <- P*W/sum(P*W), W_j = exp(-((y_tilde - y_j)^2 - min_i d_i)/(2 delta)) over P_j > 0.
+ * delta must be > 0 and finite (else PAC_E_INVAL). */
+int pac_posterior_update(pac_session* s, const double* d_y64, double y_tilde, double delta,
+                         pac_stream_t stream);
+
+/* ------------------------------------------------------------------ runtime / profiling
+ * Number of kernels this library has launched since load (all entry points). */
+uint64_t pac_launch_count(void);
+/* When enabled, pac_agg_grouped brackets its main aggregation kernel with CUDA events
+ * on `stream` and accumulates the elapsed time; pac_profile_read synchronizes on the
+ * recorded events and returns (total ms, number of timed launches), then resets. */
+int pac_profile_enable(int on);
+int pac_profile_read(double* h_total_ms, int64_t* h_launches);
+/* Library version string. */
+const char* pac_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAC_H_ */

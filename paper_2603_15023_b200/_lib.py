@@ -1,0 +1,94 @@
+"""ctypes declaration of libpac.so (include/pac.h).  Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpac.so")
+
+PAC_M = 64
+PAC_MAX_AGGS = 8
+PAC_MAX_KEYS = 4
+
+PAC_OK, PAC_E_INVAL, PAC_E_CAPACITY, PAC_E_WORKSPACE, PAC_E_CUDA, PAC_E_OVERFLOW = range(6)
+STATUS_NAMES = {0: "PAC_OK", 1: "PAC_E_INVAL", 2: "PAC_E_CAPACITY", 3: "PAC_E_WORKSPACE",
+                4: "PAC_E_CUDA", 5: "PAC_E_OVERFLOW"}
+
+COUNT, SUM_I64, SUM_F64, AVG_F64, MIN_F64, MAX_F64 = range(6)
+
+
+class PacError(RuntimeError):
+    def __init__(self, fn: str, rc: int):
+        super().__init__(f"{fn} returned {STATUS_NAMES.get(rc, rc)}")
+        self.rc = rc
+
+
+class AggSpec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("d_values", ctypes.c_void_p)]
+
+
+class KeyCol(ctypes.Structure):
+    _fields_ = [("d_col", ctypes.c_void_p), ("elem_bytes", ctypes.c_int32)]
+
+
+class Table(ctypes.Structure):
+    _fields_ = [("d_num_groups", ctypes.c_void_p), ("d_status", ctypes.c_void_p),
+                ("d_group_key", ctypes.c_void_p), ("d_rows", ctypes.c_void_p),
+                ("d_presence", ctypes.c_void_p), ("d_count", ctypes.c_void_p),
+                ("d_world", ctypes.c_void_p * PAC_MAX_AGGS)]
+
+
+_P = ctypes.c_void_p
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Loads libpac.so.  There is no fallback: a missing library is an error."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing; run `python build.py` (or __graft_entry__.build())")
+    L = ctypes.CDLL(LIB_PATH)
+    sig = {
+        "pac_session_create": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_double, ctypes.POINTER(_P)]),
+        "pac_session_destroy": (ctypes.c_int, [_P]),
+        "pac_session_query": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+        "pac_session_set_posterior": (ctypes.c_int, [_P, _P]),
+        "pac_session_posterior_device": (_P, [_P]),
+        "pac_mask": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_uint64, _P, _P]),
+        "pac_agg_workspace_size": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int64, _P]),
+        "pac_agg_grouped": (ctypes.c_int, [_P, _P, ctypes.c_uint64, _P, ctypes.c_int, _P, ctypes.c_int,
+                                           ctypes.c_int64, _P, ctypes.c_int64, _P, ctypes.c_size_t, _P]),
+        "pac_table_check": (ctypes.c_int, [_P, _P, _P]),
+        "pac_table_rederive_presence": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int64, _P]),
+        "pac_table_remap": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P, ctypes.c_int, ctypes.c_int64, _P, _P]),
+        "pac_finalize_workspace_size": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, _P]),
+        "pac_finalize": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32, _P, _P, _P,
+                                        _P, _P, ctypes.c_size_t, _P]),
+        "pac_posterior_update": (ctypes.c_int, [_P, _P, ctypes.c_double, ctypes.c_double, _P]),
+        "pac_launch_count": (ctypes.c_uint64, []),
+        "pac_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+        "pac_profile_read": (ctypes.c_int, [_P, _P]),
+        "pac_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def check(fn: str, rc: int) -> None:
+    if rc != PAC_OK:
+        raise PacError(fn, rc)
+
+
+def exported_symbols() -> list:
+    return ["pac_session_create", "pac_session_destroy", "pac_session_query", "pac_session_set_posterior",
+            "pac_session_posterior_device", "pac_mask", "pac_agg_workspace_size", "pac_agg_grouped",
+            "pac_table_check", "pac_table_rederive_presence", "pac_table_remap",
+            "pac_finalize_workspace_size", "pac_finalize", "pac_posterior_update", "pac_launch_count",
+            "pac_profile_enable", "pac_profile_read", "pac_version"]

@@ -1,0 +1,305 @@
+"""Python binding of libpac (include/pac.h): the same calls, torch tensors in, argument
+marshalling only.  Every step of the hot path runs in libpac's sm_100a kernels; this
+module only allocates device memory (torch), passes pointers and the current stream.
+
+Bit patterns (masks, packed group keys, presence K) travel in int64 tensors; use
+`as_u64` to view them as unsigned on the host.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import AVG_F64, COUNT, MAX_F64, MIN_F64, SUM_F64, SUM_I64, PAC_M, PacError, check
+
+_DEV_KEY_BYTES = {torch.int8: 1, torch.int16: 2, torch.int32: 4, torch.int64: 8}
+
+
+def _stream(dev=None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def as_u64(a) -> np.ndarray:
+    if isinstance(a, torch.Tensor):
+        a = a.detach().cpu().numpy()
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("libpac takes contiguous CUDA tensors")
+
+
+# ------------------------------------------------------------------ session (a1)
+class Session:
+    """pac_session: salt, secret world j*, posterior P on the device."""
+
+    def __init__(self, seed: int, budget: float = 1.0 / 128.0):
+        h = ctypes.c_void_p()
+        check("pac_session_create", L.lib().pac_session_create(seed & 0xFFFFFFFFFFFFFFFF, float(budget),
+                                                                 ctypes.byref(h)))
+        self._h = h
+        self.seed = seed & 0xFFFFFFFFFFFFFFFF
+        self.budget = float(budget)
+        q = self.query()
+        self.salt, self.jstar = q["salt"], q["jstar"]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def query(self) -> dict:
+        salt, js, rel, seed = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_uint64(), ctypes.c_uint64()
+        B = ctypes.c_double()
+        P = np.zeros(PAC_M, dtype=np.float64)
+        check("pac_session_query", L.lib().pac_session_query(
+            self._h, ctypes.byref(salt), ctypes.byref(js), P.ctypes.data, ctypes.byref(rel),
+            ctypes.byref(seed), ctypes.byref(B)))
+        return {"salt": salt.value, "jstar": js.value, "P": P, "releases": rel.value,
+                "seed": seed.value, "budget": B.value}
+
+    def set_posterior(self, P: np.ndarray) -> None:
+        P = np.ascontiguousarray(P, dtype=np.float64)
+        check("pac_session_set_posterior", L.lib().pac_session_set_posterior(self._h, P.ctypes.data))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            L.lib().pac_session_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ mask (a2)
+def mask(pu_keys: torch.Tensor, salt: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """pac_hash of every key: int64 tensor holding the 64-bit masks."""
+    _require_cuda(pu_keys)
+    if pu_keys.dtype != torch.int64:
+        raise ValueError("pu_keys must be int64")
+    n = pu_keys.numel()
+    if out is None:
+        out = torch.empty(n, dtype=torch.int64, device=pu_keys.device)
+    check("pac_mask", L.lib().pac_mask(_ptr(pu_keys), n, salt & 0xFFFFFFFFFFFFFFFF, _ptr(out),
+                                        _stream(pu_keys.device)))
+    return out
+
+
+# ------------------------------------------------------------------ table (a3-a5)
+@dataclass
+class PacTable:
+    kinds: List[int]
+    G_cap: int
+    num_groups: torch.Tensor
+    status: torch.Tensor
+    group_key: torch.Tensor
+    rows: torch.Tensor
+    presence: torch.Tensor
+    count: Optional[torch.Tensor]
+    world: List[Optional[torch.Tensor]]
+    _struct: Optional[L.Table] = field(default=None, repr=False)
+
+    @staticmethod
+    def allocate(kinds: Sequence[int], G_cap: int, device) -> "PacTable":
+        kinds = list(kinds)
+        mm_only = all(k in (MIN_F64, MAX_F64) for k in kinds)
+        z = lambda *s, dt=torch.int64: torch.zeros(*s, dtype=dt, device=device)
+        world = []
+        for k in kinds:
+            if k == COUNT:
+                world.append(None)
+            elif k == SUM_I64:
+                world.append(z(G_cap, PAC_M))
+            else:
+                world.append(z(G_cap, PAC_M, dt=torch.float64))
+        return PacTable(kinds, G_cap, z(1), z(1, dt=torch.int32), z(G_cap), z(G_cap), z(G_cap),
+                        None if mm_only else z(G_cap, PAC_M), world)
+
+    def struct(self) -> L.Table:
+        if self._struct is None:
+            t = L.Table()
+            t.d_num_groups = self.num_groups.data_ptr()
+            t.d_status = self.status.data_ptr()
+            t.d_group_key = self.group_key.data_ptr()
+            t.d_rows = self.rows.data_ptr()
+            t.d_presence = self.presence.data_ptr()
+            t.d_count = self.count.data_ptr() if self.count is not None else None
+            for a, w in enumerate(self.world):
+                t.d_world[a] = w.data_ptr() if w is not None else None
+            self._struct = t
+        return self._struct
+
+    def check(self) -> int:
+        """Synchronizing: number of groups; raises PacError on CAPACITY / OVERFLOW."""
+        G = ctypes.c_int64()
+        rc = L.lib().pac_table_check(ctypes.byref(self.struct()), ctypes.byref(G), _stream(self.rows.device))
+        if rc != L.PAC_OK:
+            raise PacError("pac_table_check", rc)
+        return int(G.value)
+
+    def to_host(self) -> dict:
+        G = self.check()
+        return {
+            "G": G,
+            "keys": as_u64(self.group_key[:G]),
+            "rows": self.rows[:G].cpu().numpy(),
+            "K": as_u64(self.presence[:G]),
+            "count": None if self.count is None else self.count[:G].cpu().numpy(),
+            "world": [None if w is None else w[:G].cpu().numpy() for w in self.world],
+            "kinds": list(self.kinds),
+        }
+
+
+def _agg_specs(aggs: Sequence[Tuple[int, Optional[torch.Tensor]]]):
+    arr = (L.AggSpec * max(1, len(aggs)))()
+    for a, (k, v) in enumerate(aggs):
+        if v is not None:
+            _require_cuda(v)
+            want = torch.int64 if k == SUM_I64 else torch.float64
+            if v.dtype != want:
+                raise ValueError(f"aggregate {a}: values must be {want}")
+        arr[a].kind = int(k)
+        arr[a].d_values = None if v is None else v.data_ptr()
+    return arr
+
+
+def _key_cols(keys: Sequence[torch.Tensor]):
+    arr = (L.KeyCol * max(1, len(keys)))()
+    for c, k in enumerate(keys):
+        _require_cuda(k)
+        if k.dtype not in _DEV_KEY_BYTES:
+            raise ValueError("group key columns must be int8/16/32/64")
+        arr[c].d_col = k.data_ptr()
+        arr[c].elem_bytes = _DEV_KEY_BYTES[k.dtype]
+    return arr
+
+
+class Aggregator:
+    """pac_agg_grouped with a cached workspace and output table (reused across calls)."""
+
+    def __init__(self, kinds: Sequence[int], G_cap: int, device="cuda"):
+        self.kinds = list(kinds)
+        self.G_cap = int(G_cap)
+        self.device = torch.device(device)
+        self.table = PacTable.allocate(self.kinds, self.G_cap, self.device)
+        self._ws = None
+
+    def _workspace(self, specs, n_aggs):
+        nb = ctypes.c_size_t()
+        check("pac_agg_workspace_size", L.lib().pac_agg_workspace_size(specs, n_aggs, self.G_cap,
+                                                                         ctypes.byref(nb)))
+        if self._ws is None or self._ws.numel() < nb.value:
+            self._ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=self.device)
+        return self._ws, nb.value
+
+    def __call__(self, values: Sequence[Optional[torch.Tensor]], keys: Sequence[torch.Tensor] = (),
+                 pu_key: Optional[torch.Tensor] = None, mask: Optional[torch.Tensor] = None,
+                 salt: int = 0) -> PacTable:
+        if len(values) != len(self.kinds):
+            raise ValueError("one value tensor (or None for COUNT) per aggregate")
+        aggs = list(zip(self.kinds, values))
+        specs = _agg_specs(aggs)
+        kc = _key_cols(keys)
+        _require_cuda(pu_key, mask)
+        n = (pu_key if pu_key is not None else mask).numel()
+        ws, nb = self._workspace(specs, len(aggs))
+        t = self.table
+        check("pac_agg_grouped", L.lib().pac_agg_grouped(
+            _ptr(pu_key), _ptr(mask), salt & 0xFFFFFFFFFFFFFFFF, kc, len(keys), specs, len(aggs), n,
+            ctypes.byref(t.struct()), self.G_cap, _ptr(ws), nb, _stream(self.device)))
+        return t
+
+
+def agg_grouped(aggs: Sequence[Tuple[int, Optional[torch.Tensor]]], keys: Sequence[torch.Tensor] = (),
+                pu_key: Optional[torch.Tensor] = None, mask: Optional[torch.Tensor] = None, salt: int = 0,
+                G_cap: int = 1024) -> PacTable:
+    dev = (pu_key if pu_key is not None else mask).device
+    ag = Aggregator([k for k, _ in aggs], G_cap, dev)
+    return ag([v for _, v in aggs], keys, pu_key=pu_key, mask=mask, salt=salt)
+
+
+def rederive_presence(table: PacTable, aggs) -> None:
+    specs = _agg_specs([(k, v) for k, v in aggs])
+    check("pac_table_rederive_presence", L.lib().pac_table_rederive_presence(
+        ctypes.byref(table.struct()), specs, len(aggs), table.G_cap, _stream(table.rows.device)))
+
+
+def remap(table: PacTable, union_keys: torch.Tensor, aggs) -> PacTable:
+    """Lay `table` out on the ascending union dictionary `union_keys` (int64 bit patterns)."""
+    Gu = union_keys.numel()
+    out = PacTable.allocate(table.kinds, max(Gu, 1), table.rows.device)
+    specs = _agg_specs([(k, v) for k, v in aggs])
+    check("pac_table_remap", L.lib().pac_table_remap(
+        ctypes.byref(table.struct()), _ptr(union_keys), Gu, specs, len(aggs), table.G_cap,
+        ctypes.byref(out.struct()), _stream(table.rows.device)))
+    return out
+
+
+# ------------------------------------------------------------------ finalize (a6, a7)
+class Finalizer:
+    """pac_finalize with cached workspace/outputs."""
+
+    def __init__(self, kinds: Sequence[int], G_cap: int, device="cuda"):
+        self.kinds = list(kinds)
+        self.G_cap = int(G_cap)
+        dev = torch.device(device)
+        A = len(self.kinds)
+        nb = ctypes.c_size_t()
+        check("pac_finalize_workspace_size", L.lib().pac_finalize_workspace_size(self.G_cap, A,
+                                                                                   ctypes.byref(nb)))
+        self.ws = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+        self.ws_bytes = nb.value
+        self.release = torch.empty(self.G_cap, A, dtype=torch.float64, device=dev)
+        self.is_null = torch.empty(self.G_cap, A, dtype=torch.uint8, device=dev)
+        self.flags = torch.empty(self.G_cap, dtype=torch.uint8, device=dev)
+        self.delta = torch.empty(self.G_cap, A, dtype=torch.float64, device=dev)
+
+    def __call__(self, session: Session, table: PacTable, round_: int = 0):
+        specs = _agg_specs([(k, w) for k, w in zip(table.kinds, table.world)])
+        check("pac_finalize", L.lib().pac_finalize(
+            session.handle, ctypes.byref(table.struct()), specs, len(self.kinds), self.G_cap, int(round_),
+            _ptr(self.release), _ptr(self.is_null), _ptr(self.flags), _ptr(self.delta), _ptr(self.ws),
+            self.ws_bytes, _stream(self.release.device)))
+        return self.release, self.is_null, self.flags, self.delta
+
+
+def finalize(session: Session, table: PacTable, round_: int = 0):
+    return Finalizer(table.kinds, table.G_cap, table.rows.device)(session, table, round_)
+
+
+def posterior_update(session: Session, y64: torch.Tensor, y_tilde: float, delta: float) -> None:
+    _require_cuda(y64)
+    check("pac_posterior_update", L.lib().pac_posterior_update(session.handle, _ptr(y64), float(y_tilde),
+                                                                float(delta), _stream(y64.device)))
+
+
+# ------------------------------------------------------------------ runtime
+def launch_count() -> int:
+    return int(L.lib().pac_launch_count())
+
+
+def profile_enable(on: bool) -> None:
+    L.lib().pac_profile_enable(1 if on else 0)
+
+
+def profile_read() -> Tuple[float, int]:
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    check("pac_profile_read", L.lib().pac_profile_read(ctypes.byref(ms), ctypes.byref(n)))
+    return float(ms.value), int(n.value)
+
+
+def version() -> str:
+    return L.lib().pac_version().decode()
