@@ -202,7 +202,8 @@ def main():
     keys = cols["keys"]
     vals = [None if i < 0 else cols["values"][i] for _, i in w.aggs]
     kinds = [k for k, _ in w.aggs]
-    G_cap = 64 if w.name in ("C1", "C2") else (4096 if w.name in ("C4", "C5") else 1 << 21)
+    # capacity hints from the key domains of the synthetic configs (R20 packed keys)
+    G_cap = {"C1": 1, "C2": 16, "C4": 1024, "C5": 128}.get(w.name, 1 << 21)
     seed = 0x5EED
     sess = pac.Session(seed, w.budget)
     ag = pac.Aggregator(kinds, G_cap, dev)

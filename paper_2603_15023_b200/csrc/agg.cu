@@ -2,7 +2,7 @@
 //
 // Design:
 //  * k_mask: row-parallel pac_hash.
-//  * k_agg_smem<NI,NF,MM>: persistent CTAs over contiguous row ranges, tiles of T rows.
+//  * k_agg_tiles<NI,NF,MM>: persistent CTAs over contiguous row ranges, tiles of T rows.
 //      phase A (row-parallel): fused pac_hash, group key packing, CTA-local slot lookup
 //               (smem dictionary in front of the HBM dictionary), rows staged in smem;
 //      phase B: counting sort of the tile's rows by local slot;
@@ -21,7 +21,8 @@
 
 namespace pac {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 512;      // k_agg_minmax
+constexpr int kTileThreads = 256;  // k_agg_tiles: 128-register budget (2 CTAs / SM)
 constexpr int kOvfBase = 0x20000000;  // local-dict code for keys without a local slot
 constexpr int kSmallSort = 4096;      // single-CTA bitonic sort up to this many groups
 
@@ -54,9 +55,10 @@ struct AggPlan {
 };
 
 struct SmemLayout {
-  int T, Lcap, LH;
+  int T, TS, Lcap, LH;
   int o_lkey, o_lstate, o_lprov, o_lrows, o_cnt, o_isum, o_fsum, o_min, o_max;
-  int o_mask, o_slot, o_order, o_ival, o_fval, o_mval, o_hist, o_offs, o_runoffs, o_misc;
+  int o_mask, o_slot, o_rank, o_ucnt, o_queue, o_ival, o_i32, o_fval, o_mval, o_hist, o_offs,
+      o_runoffs, o_tcs, o_misc;
   int bytes;
 };
 
@@ -64,7 +66,10 @@ struct Misc {
   int nlocal;   // local slots handed out
   int ndict;    // local dictionary reservations
   int nruns;    // runs in the current tile
-  int pad;
+  int big;        // some int64 value of the tile has |v| >= 2^26 (no int32 tables)
+  int nqueue;     // rows whose mask needs more than one draw word
+  int nonfinite;  // some f64 value of the tile is inf/nan (no 0/1-FMA tables)
+  int pad[2];
 };
 
 // ------------------------------------------------------------------ dictionaries
@@ -114,7 +119,7 @@ __device__ int global_slot(const AggPlan& p, uint64_t key) {
 // key that has no local slot (its rows go straight to the HBM table; prov -1 = dropped).
 __device__ int local_code(const AggPlan& p, uint64_t key, unsigned long long* lkey, int* lstate,
                           int LH, int* lprov, int Lcap, Misc* misc) {
-  uint32_t h = dict_hash(key) & (LH - 1);
+  uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 40) & (LH - 1);
   for (;;) {
     int st = *(volatile int*)&lstate[h];
     if (st == 0) {
@@ -188,25 +193,68 @@ __global__ void __launch_bounds__(256) k_mask(const long long* __restrict__ key,
     out[i] = pac_hash_dev((uint64_t)__ldg(key + i), salt);
 }
 
-// ------------------------------------------------------------------ k_agg_smem
+// ------------------------------------------------------------------ k_agg_tiles (v3)
+// Bit-matrix transpose of a 32-row run: on input lane r holds row r's
+// 32-bit mask word; on output lane c holds the pattern of world c over the run.  Stage s
+// swaps the off-diagonal s x s blocks: the partner's word is rotated by s (low lane) or
+// 32-s (high lane) with one funnel shift and merged with one LOP3 under a per-lane mask.
+// Per-lane constants of the 5 stages live in shared memory (tcs[stage*32 + lane] =
+// {keep mask, rotate amount}), loaded once per run: cheaper than rematerialising them.
+__device__ __forceinline__ uint2 transpose_const(int lane, int i) {
+  const int s = 16 >> i;
+  const uint32_t M = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
+                   : s == 2 ? 0x33333333u : 0x55555555u;
+  const bool up = (lane & s) != 0;
+  return make_uint2(up ? ~M : M, (uint32_t)(up ? 32 - s : s));
+}
+
+__device__ __forceinline__ void transpose2x32(uint32_t& a, uint32_t& b, const uint2* __restrict__ tcs,
+                                              int lane) {
+  uint2 c[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) c[i] = tcs[i * 32 + lane];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int s = 16 >> i;
+    const uint32_t ya = __shfl_xor_sync(0xffffffffu, a, s);
+    const uint32_t yb = __shfl_xor_sync(0xffffffffu, b, s);
+    a = (a & c[i].x) | (__funnelshift_l(ya, ya, c[i].y) & ~c[i].x);
+    b = (b & c[i].x) | (__funnelshift_l(yb, yb, c[i].y) & ~c[i].x);
+  }
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src) {
+  const int lo = __shfl_sync(0xffffffffu, __double2loint(v), src);
+  const int hi = __shfl_sync(0xffffffffu, __double2hiint(v), src);
+  return __hiloint2double(hi, lo);
+}
+
+__device__ __forceinline__ bool finite_bits(double v) {
+  return (__double2hiint(v) & 0x7FF00000) != 0x7FF00000;
+}
+
 template <int NI, int NF, int MM>
-__global__ void __launch_bounds__(kThreads, 2) k_agg_smem(AggPlan p, SmemLayout L) {
+__global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLayout L) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* lkey = (unsigned long long*)(smem + L.o_lkey);
   int* lstate = (int*)(smem + L.o_lstate);
   int* lprov = (int*)(smem + L.o_lprov);
   unsigned long long* lrows = (unsigned long long*)(smem + L.o_lrows);
-  unsigned long long* cnt = (unsigned long long*)(smem + L.o_cnt);
+  unsigned* cnt = (unsigned*)(smem + L.o_cnt);
   unsigned long long* isum = (unsigned long long*)(smem + L.o_isum);
   double* fsum = (double*)(smem + L.o_fsum);
   long long* emin = (long long*)(smem + L.o_min);
   long long* emax = (long long*)(smem + L.o_max);
-  unsigned long long* smask = (unsigned long long*)(smem + L.o_mask);
-  unsigned short* sslot = (unsigned short*)(smem + L.o_slot);
-  unsigned short* order = (unsigned short*)(smem + L.o_order);
-  long long* sival = (long long*)(smem + L.o_ival);
-  double* sfval = (double*)(smem + L.o_fval);
-  double* smval = (double*)(smem + L.o_mval);
+  unsigned long long* smask = (unsigned long long*)(smem + L.o_mask);  // [TS] slot-sorted
+  long long* sival = (long long*)(smem + L.o_ival);                     // [NI][TS]
+  int* si32 = (int*)(smem + L.o_i32);                                   // [NI][TS]
+  double* sfval = (double*)(smem + L.o_fval);                           // [NF][TS]
+  double* smval = (double*)(smem + L.o_mval);                           // [TS]
+  unsigned short* sslot = (unsigned short*)(smem + L.o_slot);           // [T]
+  unsigned char* srank = (unsigned char*)(smem + L.o_rank);             // [T]
+  unsigned short* ucnt = (unsigned short*)(smem + L.o_ucnt);            // [units][Lcap]
+  unsigned short* qpos = (unsigned short*)(smem + L.o_queue);           // [T]
+  unsigned short* qrow = qpos + L.T;                                    // [T]
   int* hist = (int*)(smem + L.o_hist);
   int* offs = (int*)(smem + L.o_offs);
   int* runoffs = (int*)(smem + L.o_runoffs);
@@ -214,8 +262,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_agg_smem(AggPlan p, SmemLayout 
 
   const int tid = threadIdx.x, nth = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
-  const int T = L.T, Lcap = L.Lcap, LH = L.LH;
+  const int T = L.T, TS = L.TS, Lcap = L.Lcap, LH = L.LH;
+  const int units = T >> 5;
   const unsigned short kNone = 0xFFFF;
+  const unsigned lt_mask = (1u << lane) - 1u;
 
   for (int i = tid; i < LH; i += nth) lstate[i] = 0;
   for (int i = tid; i < Lcap; i += nth) lrows[i] = 0;
@@ -235,73 +285,126 @@ __global__ void __launch_bounds__(kThreads, 2) k_agg_smem(AggPlan p, SmemLayout 
   unsigned long long maxabs = 0;
   __syncthreads();
 
-  // contiguous row range of this CTA, in whole tiles
   const int64_t ntiles = (p.n_rows + T - 1) / T;
   const int64_t t_per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * t_per;
   const int64_t t1 = min(ntiles, t0 + t_per);
 
+  // run-processing state of this warp (lane: worlds lane and lane+32)
+  uint2* tcs = (uint2*)(smem + L.o_tcs);
+  if (tid < 32) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) tcs[i * 32 + tid] = transpose_const(tid, i);
+  }
+  const int sub = lane & 15;          // subset of this lane's 16-entry table
+  const int tsrc = (lane >> 4) << 2;  // lanes 0-15: rows 8q..8q+3; lanes 16-31: rows 8q+4..8q+7
+  const int ib0 = sub & 1, ib1 = (sub >> 1) & 1, ib2 = (sub >> 2) & 1, ib3 = (sub >> 3) & 1;
+  int cur = -1;
+  unsigned c0 = 0, c1 = 0;
+  long long ia0[NI > 0 ? NI : 1], ia1[NI > 0 ? NI : 1];
+  double fa0[NF > 0 ? NF : 1], fa1[NF > 0 ? NF : 1];
+  double mn0 = INFINITY, mn1 = INFINITY, mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < NI; ++c) ia0[c] = ia1[c] = 0;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) fa0[c] = fa1[c] = 0.0;
+
+  auto flush = [&]() {
+    if (cur < 0) return;
+    const size_t b = (size_t)cur * kM;
+    if (c0) atomicAdd(&cnt[b + lane], c0);
+    if (c1) atomicAdd(&cnt[b + lane + 32], c1);
+#pragma unroll
+    for (int c = 0; c < NI; ++c) {
+      atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane], (unsigned long long)ia0[c]);
+      atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane + 32], (unsigned long long)ia1[c]);
+      ia0[c] = ia1[c] = 0;
+    }
+#pragma unroll
+    for (int c = 0; c < NF; ++c) {
+      atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane], fa0[c]);
+      atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane + 32], fa1[c]);
+      fa0[c] = fa1[c] = 0.0;
+    }
+    if (MM & 1) {
+      atomicMin(&emin[b + lane], enc_f64(mn0));
+      atomicMin(&emin[b + lane + 32], enc_f64(mn1));
+    }
+    if (MM & 2) {
+      atomicMax(&emax[b + lane], enc_f64(mx0));
+      atomicMax(&emax[b + lane + 32], enc_f64(mx1));
+    }
+    c0 = c1 = 0;
+    mn0 = mn1 = INFINITY;
+    mx0 = mx1 = -INFINITY;
+  };
+
   for (int64_t tile = t0; tile < t1; ++tile) {
     const int64_t base = tile * T;
     const int tn = (int)min((int64_t)T, p.n_rows - base);
-    for (int i = tid; i < Lcap; i += nth) hist[i] = 0;
+    for (int i = tid; i < units * Lcap; i += nth) ucnt[i] = 0;
+    if (tid == 0) {
+      misc->big = 0;
+      misc->nonfinite = 0;
+      misc->nqueue = 0;
+    }
     __syncthreads();
 
-    // ---------------- phase A: row-parallel hash, slot, staging
+    // ---------------- A1: group slot of every row + rank within its 32-row unit
     for (int li = tid; li < T; li += nth) {
-      unsigned short code16 = kNone;
+      int s = -1;
       if (li < tn) {
         const int64_t r = base + li;
-        uint64_t m = p.mask_in ? (uint64_t)__ldg(p.mask_in + r)
-                               : pac_hash_dev((uint64_t)__ldg(p.pu_key + r), p.salt);
-        long long iv[NI > 0 ? NI : 1];
-        double fv[NF > 0 ? NF : 1];
-        double mv = 0.0;
-#pragma unroll
-        for (int c = 0; c < NI; ++c) {
-          iv[c] = __ldg(p.icol[c] + r);
-          unsigned long long a = iv[c] < 0 ? 0ull - (unsigned long long)iv[c] : (unsigned long long)iv[c];
-          maxabs = a > maxabs ? a : maxabs;
-        }
-#pragma unroll
-        for (int c = 0; c < NF; ++c) fv[c] = __ldg(p.fcol[c] + r);
-        if (MM) mv = __ldg(p.mcol + r);
-        if (m != 0) {
-          uint64_t key = row_group_key(p, r);
-          int code = local_code(p, key, lkey, lstate, LH, lprov, Lcap, misc);
+        bool keep = true;
+        if (p.mask_in) keep = __ldg(p.mask_in + r) != 0ull;  // R21: a row in no world is dropped
+        if (keep) {
+          const uint64_t key = row_group_key(p, r);
+          const int code = local_code(p, key, lkey, lstate, LH, lprov, Lcap, misc);
           if (code < kOvfBase) {
-            int s = code - 1;
-            code16 = (unsigned short)s;
-            smask[li] = m;
+            s = code - 1;
+          } else {  // no local slot: straight to the HBM table (rare)
+            long long iv[NI > 0 ? NI : 1];
+            double fv[NF > 0 ? NF : 1];
 #pragma unroll
-            for (int c = 0; c < NI; ++c) sival[c * T + li] = iv[c];
+            for (int c = 0; c < NI; ++c) iv[c] = __ldg(p.icol[c] + r);
 #pragma unroll
-            for (int c = 0; c < NF; ++c) sfval[c * T + li] = fv[c];
-            if (MM) smval[li] = mv;
-            atomicAdd(&hist[s], 1);
-          } else {
+            for (int c = 0; c < NF; ++c) fv[c] = __ldg(p.fcol[c] + r);
+            const double mv = MM ? __ldg(p.mcol + r) : 0.0;
+            const uint64_t m = p.mask_in ? (uint64_t)__ldg(p.mask_in + r)
+                                         : pac_hash_dev((uint64_t)__ldg(p.pu_key + r), p.salt);
             global_row_update<NI, NF, MM>(p, code - kOvfBase - 1, m, iv, fv, mv);
           }
         }
       }
-      sslot[li] = code16;
+      const unsigned peers = __match_any_sync(0xffffffffu, s >= 0 ? (unsigned)s : 0x10000u + lane);
+      if (s >= 0) {
+        srank[li] = (unsigned char)__popc(peers & lt_mask);
+        if ((peers & lt_mask) == 0) ucnt[(li >> 5) * Lcap + s] = (unsigned short)__popc(peers);
+      }
+      sslot[li] = s >= 0 ? (unsigned short)s : kNone;
     }
     __syncthreads();
 
-    // ---------------- phase B: offsets and run offsets (warp 0), then stable-enough scatter
+    // ---------------- B: slot totals, 8-row padded offsets, run offsets, unit positions
+    for (int s = tid; s < Lcap; s += nth) {
+      int tot = 0;
+      for (int u = 0; u < units; ++u) tot += ucnt[u * Lcap + s];
+      hist[s] = tot;
+    }
+    __syncthreads();
     if (wid == 0) {
       const int per = (Lcap + 31) / 32;
       const int s0 = lane * per;
       int hsum = 0, rsum = 0;
       for (int s = s0; s < min(Lcap, s0 + per); ++s) {
-        hsum += hist[s];
+        hsum += (hist[s] + 7) & ~7;
         rsum += (hist[s] + 31) >> 5;
       }
       int hx = hsum, rx = rsum;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        int a = __shfl_up_sync(0xffffffffu, hx, d);
-        int b = __shfl_up_sync(0xffffffffu, rx, d);
+        const int a = __shfl_up_sync(0xffffffffu, hx, d);
+        const int b = __shfl_up_sync(0xffffffffu, rx, d);
         if (lane >= d) {
           hx += a;
           rx += b;
@@ -313,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_agg_smem(AggPlan p, SmemLayout 
         offs[s] = hx;
         runoffs[s] = rx;
         lrows[s] += (unsigned long long)hist[s];
-        hx += hist[s];
+        hx += (hist[s] + 7) & ~7;
         rx += (hist[s] + 31) >> 5;
       }
       if (lane == 31) {
@@ -322,115 +425,204 @@ __global__ void __launch_bounds__(kThreads, 2) k_agg_smem(AggPlan p, SmemLayout 
       }
     }
     __syncthreads();
-    // scatter: hist doubles as the per-slot cursor (offs + cursor)
-    for (int i = tid; i < Lcap; i += nth) hist[i] = offs[i];
-    __syncthreads();
-    for (int li = tid; li < tn; li += nth) {
-      unsigned short s = sslot[li];
-      if (s != kNone) order[atomicAdd(&hist[s], 1)] = (unsigned short)li;
+    for (int s = tid; s < Lcap; s += nth) {
+      const int o0 = offs[s];
+      int o = o0;
+      for (int u = 0; u < units; ++u) {
+        const int c = ucnt[u * Lcap + s];
+        ucnt[u * Lcap + s] = (unsigned short)o;
+        o += c;
+      }
+      // zero the padding rows up to the next multiple of 8 (mask 0 = in no world)
+      for (int q = o; q < o0 + ((hist[s] + 7) & ~7); ++q) {
+        smask[q] = 0;
+#pragma unroll
+        for (int c = 0; c < NI; ++c) {
+          sival[c * TS + q] = 0;
+          si32[c * TS + q] = 0;
+        }
+#pragma unroll
+        for (int c = 0; c < NF; ++c) sfval[c * TS + q] = 0.0;
+        if (MM) smval[q] = 0.0;
+      }
     }
     __syncthreads();
 
-    // ---------------- phase C: world-parallel runs
-    {
-      const int R = misc->nruns;
-      const int r0 = (int)(((long long)R * wid) / nw);
-      const int r1 = (int)(((long long)R * (wid + 1)) / nw);
-      int cur = -1;
-      unsigned c0 = 0, c1 = 0;
-      long long i0[NI > 0 ? NI : 1], i1[NI > 0 ? NI : 1];
-      double f0[NF > 0 ? NF : 1], f1[NF > 0 ? NF : 1];
-      double mn0 = INFINITY, mn1 = INFINITY, mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < NI; ++c) i0[c] = i1[c] = 0;
-#pragma unroll
-      for (int c = 0; c < NF; ++c) f0[c] = f1[c] = 0.0;
-
-      auto flush = [&](int s) {
-        if (s < 0) return;
-        const size_t b = (size_t)s * kM;
-        atomicAdd(&cnt[b + lane], (unsigned long long)c0);
-        atomicAdd(&cnt[b + lane + 32], (unsigned long long)c1);
+    // ---------------- A2: hash + values, written straight to the slot-sorted position.
+    // pac_hash runs its first draw word inline; rows still needing flips are queued.
+    bool big = false, nonfin = false;
+    for (int li = tid; li < T; li += nth) {
+      const unsigned short s = sslot[li];
+      bool pending = false;
+      int pos = 0;
+      if (s != kNone) {
+        const int64_t r = base + li;
+        pos = ucnt[(li >> 5) * Lcap + s] + srank[li];
+        uint64_t m;
+        if (p.mask_in) {
+          m = (uint64_t)__ldg(p.mask_in + r);
+        } else {
+          const HashState h = pac_hash_begin((uint64_t)__ldg(p.pu_key + r), p.salt);
+          m = h.x ^ (((__popcll(h.x) > 32) ? h.x : ~h.x) ^ h.cand);
+          pending = h.k > 0;
+        }
+        smask[pos] = m;
 #pragma unroll
         for (int c = 0; c < NI; ++c) {
-          atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane], (unsigned long long)i0[c]);
-          atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane + 32], (unsigned long long)i1[c]);
+          const long long v = __ldg(p.icol[c] + r);
+          const unsigned long long a = v < 0 ? 0ull - (unsigned long long)v : (unsigned long long)v;
+          maxabs = a > maxabs ? a : maxabs;
+          big |= a >= (1ull << 26);
+          sival[c * TS + pos] = v;
+          si32[c * TS + pos] = (int)v;
         }
 #pragma unroll
         for (int c = 0; c < NF; ++c) {
-          atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane], f0[c]);
-          atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane + 32], f1[c]);
+          const double v = __ldg(p.fcol[c] + r);
+          nonfin |= !finite_bits(v);
+          sfval[c * TS + pos] = v;
         }
-        if (MM & 1) {
-          atomicMin(&emin[b + lane], enc_f64(mn0));
-          atomicMin(&emin[b + lane + 32], enc_f64(mn1));
-        }
-        if (MM & 2) {
-          atomicMax(&emax[b + lane], enc_f64(mx0));
-          atomicMax(&emax[b + lane + 32], enc_f64(mx1));
-        }
-        c0 = c1 = 0;
-#pragma unroll
-        for (int c = 0; c < NI; ++c) i0[c] = i1[c] = 0;
-#pragma unroll
-        for (int c = 0; c < NF; ++c) f0[c] = f1[c] = 0.0;
-        mn0 = mn1 = INFINITY;
-        mx0 = mx1 = -INFINITY;
-      };
+        if (MM) smval[pos] = __ldg(p.mcol + r);
+      }
+      const unsigned pm = __ballot_sync(0xffffffffu, pending);
+      int qb = 0;
+      if (lane == 0 && pm) qb = atomicAdd(&misc->nqueue, __popc(pm));
+      qb = __shfl_sync(0xffffffffu, qb, 0) + __popc(pm & lt_mask);
+      if (pending) {
+        qpos[qb] = (unsigned short)pos;
+        qrow[qb] = (unsigned short)li;
+      }
+    }
+    if (NI > 0 && __any_sync(0xffffffffu, big) && lane == 0) misc->big = 1;
+    if (NF > 0 && __any_sync(0xffffffffu, nonfin) && lane == 0) misc->nonfinite = 1;
+    __syncthreads();
 
+    // ---------------- A3: finish the queued masks.  State re-derived from the key and the
+    // partial mask: cand = majority positions of the current word, k = |popcount - 32|.
+    // One extra draw word for every queued row (branch-free), then a loop for the few left.
+    {
+      const int qn = misc->nqueue;
+      for (int qi = tid; qi < qn; qi += nth) {
+        const int pos = qpos[qi];
+        const uint64_t x = fmix64((uint64_t)__ldg(p.pu_key + base + qrow[qi]) ^ p.salt);
+        const uint64_t m = smask[pos];
+        smask[pos] = pac_hash_finish(x, (__popcll(x) > 32) ? m : ~m, abs(__popcll(m) - 32));
+      }
+    }
+    __syncthreads();
+
+    // ---------------- C: world-parallel runs, transposed "Four Russians" tables
+    {
+      const bool small = (NI == 0) || misc->big == 0;
+      const bool fin = (NF == 0) || misc->nonfinite == 0;
+      const int R = misc->nruns;
+      const int r0 = (int)(((long long)R * wid) / nw);
+      const int r1 = (int)(((long long)R * (wid + 1)) / nw);
       int s = 0;
       if (r0 < r1) {
-        int lo = 0, hi = Lcap;  // last s with runoffs[s] <= r0
+        int lo = 0, hi = Lcap;
         while (lo < hi) {
-          int mid = (lo + hi + 1) >> 1;
+          const int mid = (lo + hi + 1) >> 1;
           if (runoffs[mid] <= r0) lo = mid; else hi = mid - 1;
         }
         s = lo;
       }
+      const double db0 = ib0, db1 = ib1, db2 = ib2, db3 = ib3;
       for (int r = r0; r < r1; ++r) {
         while (runoffs[s + 1] <= r) ++s;
         if (s != cur) {
-          flush(cur);
+          flush();
           cur = s;
         }
-        const int beg = offs[s] + 32 * (r - runoffs[s]);
-        const int len = min(32, offs[s] + (hist[s] - offs[s]) - beg);
-        for (int k = 0; k < len; ++k) {
-          const int li = order[beg + k];
-          const uint64_t m = smask[li];
-          const bool b0 = (m >> lane) & 1ull;
-          const bool b1 = (m >> (lane + 32)) & 1ull;
-          c0 += b0;
-          c1 += b1;
+        const int k0 = 32 * (r - runoffs[s]);
+        const int beg = offs[s] + k0;
+        const int len = min(32, hist[s] - k0);
+        const uint64_t m = lane < len ? smask[beg + lane] : 0ull;
+        uint32_t P = (uint32_t)m, Q = (uint32_t)(m >> 32);
+        transpose2x32(P, Q, tcs, lane);
+        c0 += __popc(P);
+        c1 += __popc(Q);
+        // nibble indices: table A (lanes 0-15) covers rows 8q..8q+3, B (16-31) rows 8q+4..8q+7;
+        // shfl uses only the low 5 bits of the source lane.
+        const uint32_t PA = P & 0x0F0F0F0Fu, PB = ((P >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
+        const uint32_t QA = Q & 0x0F0F0F0Fu, QB = ((Q >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
+        const int nq = (len + 7) >> 3;
+        int rs0[NI > 0 ? NI : 1], rs1[NI > 0 ? NI : 1];
+#pragma unroll
+        for (int c = 0; c < NI; ++c) rs0[c] = rs1[c] = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q >= nq) break;
+          const int a0 = (int)(PA >> (8 * q)), b0 = (int)(PB >> (8 * q));
+          const int a1 = (int)(QA >> (8 * q)), b1 = (int)(QB >> (8 * q));
+          const int row = beg + 8 * q + tsrc;
 #pragma unroll
           for (int c = 0; c < NI; ++c) {
-            const long long v = sival[c * T + li];
-            if (b0) i0[c] += v;
-            if (b1) i1[c] += v;
+            if (small) {
+              const int4 v = *(const int4*)(si32 + c * TS + row);
+              const int t = v.x * ib0 + v.y * ib1 + v.z * ib2 + v.w * ib3;
+              rs0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
+              rs1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
+            } else {
+              const longlong2 u = *(const longlong2*)(sival + c * TS + row);
+              const longlong2 w = *(const longlong2*)(sival + c * TS + row + 2);
+              const long long t = u.x * ib0 + u.y * ib1 + w.x * ib2 + w.y * ib3;
+              ia0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
+              ia1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
+            }
           }
 #pragma unroll
           for (int c = 0; c < NF; ++c) {
-            const double v = sfval[c * T + li];
-            if (b0) f0[c] += v;
-            if (b1) f1[c] += v;
+            const double2 u = *(const double2*)(sfval + c * TS + row);
+            const double2 w = *(const double2*)(sfval + c * TS + row + 2);
+            double t;
+            if (fin) {  // exact: 0*v + t == t and 1*v + t == v + t for finite v
+              t = fma(db3, w.y, fma(db2, w.x, fma(db1, u.y, db0 * u.x)));
+            } else {
+              t = ib0 ? u.x : 0.0;
+              if (ib1) t += u.y;
+              if (ib2) t += w.x;
+              if (ib3) t += w.y;
+            }
+            fa0[c] += shfl_d(t, a0);
+            fa0[c] += shfl_d(t, b0);
+            fa1[c] += shfl_d(t, a1);
+            fa1[c] += shfl_d(t, b1);
           }
           if (MM) {
-            const double v = smval[li];
+            const double2 u = *(const double2*)(smval + row);
+            const double2 w = *(const double2*)(smval + row + 2);
             if (MM & 1) {
-              if (b0) mn0 = fmin(mn0, v);
-              if (b1) mn1 = fmin(mn1, v);
+              double t = ib0 ? u.x : INFINITY;
+              if (ib1) t = fmin(t, u.y);
+              if (ib2) t = fmin(t, w.x);
+              if (ib3) t = fmin(t, w.y);
+              mn0 = fmin(mn0, fmin(shfl_d(t, a0), shfl_d(t, b0)));
+              mn1 = fmin(mn1, fmin(shfl_d(t, a1), shfl_d(t, b1)));
             }
             if (MM & 2) {
-              if (b0) mx0 = fmax(mx0, v);
-              if (b1) mx1 = fmax(mx1, v);
+              double t = ib0 ? u.x : -INFINITY;
+              if (ib1) t = fmax(t, u.y);
+              if (ib2) t = fmax(t, w.x);
+              if (ib3) t = fmax(t, w.y);
+              mx0 = fmax(mx0, fmax(shfl_d(t, a0), shfl_d(t, b0)));
+              mx1 = fmax(mx1, fmax(shfl_d(t, a1), shfl_d(t, b1)));
             }
           }
         }
+        if (small) {
+#pragma unroll
+          for (int c = 0; c < NI; ++c) {
+            ia0[c] += rs0[c];
+            ia1[c] += rs1[c];
+          }
+        }
       }
-      flush(cur);
     }
     __syncthreads();
   }
+  flush();
+  __syncthreads();
 
   // ---------------- CTA table -> provisional HBM table
   const int nloc = min(misc->nlocal, Lcap);
@@ -439,15 +631,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_agg_smem(AggPlan p, SmemLayout 
     const int prov = lprov[s];
     if (prov < 0) continue;
     const size_t g = (size_t)prov * kM + (i % kM);
-    if (cnt[i]) atomicAdd(&p.prov_count[g], cnt[i]);
+    if (cnt[i]) atomicAdd(&p.prov_count[g], (unsigned long long)cnt[i]);
 #pragma unroll
     for (int c = 0; c < NI; ++c) {
-      unsigned long long v = isum[(size_t)c * Lcap * kM + i];
+      const unsigned long long v = isum[(size_t)c * Lcap * kM + i];
       if (v) atomicAdd(&p.prov_isum[c][g], v);
     }
 #pragma unroll
     for (int c = 0; c < NF; ++c) {
-      double v = fsum[(size_t)c * Lcap * kM + i];
+      const double v = fsum[(size_t)c * Lcap * kM + i];
       if (v != 0.0) atomicAdd(&p.prov_fsum[c][g], v);
     }
     if (MM & 1) atomicMin(&p.prov_min[g], emin[i]);
@@ -458,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_agg_smem(AggPlan p, SmemLayout 
   if (NI > 0) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
-      unsigned long long o = __shfl_xor_sync(0xffffffffu, maxabs, d);
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, maxabs, d);
       maxabs = o > maxabs ? o : maxabs;
     }
     if (lane == 0 && maxabs) atomicMax(p.gmaxabs, maxabs);
@@ -889,6 +1081,7 @@ static WsLayout ws_layout(const AccSet& A, int64_t G_cap) {
 static SmemLayout make_layout(const AccSet& A, int T, int Lcap) {
   SmemLayout L{};
   L.T = T;
+  L.TS = T + 8 * Lcap;  // slot-sorted staging, each slot padded to a multiple of 8 rows
   L.Lcap = Lcap;
   L.LH = (int)next_pow2(std::max(4 * Lcap, 256));
   int off = 0;
@@ -898,35 +1091,48 @@ static SmemLayout make_layout(const AccSet& A, int T, int Lcap) {
     return o;
   };
   const bool mm = A.has_min || A.has_max;
-  L.o_cnt = take(Lcap * kM * 8);
+  const int TS = L.TS;
   L.o_isum = take(A.ni * Lcap * kM * 8);
   L.o_fsum = take(A.nf * Lcap * kM * 8);
   L.o_min = take(A.has_min ? Lcap * kM * 8 : 0);
   L.o_max = take(A.has_max ? Lcap * kM * 8 : 0);
   L.o_lrows = take(Lcap * 8);
   L.o_lkey = take(L.LH * 8);
-  L.o_mask = take(T * 8);
-  L.o_ival = take(A.ni * T * 8);
-  L.o_fval = take(A.nf * T * 8);
-  L.o_mval = take(mm ? T * 8 : 0);
+  L.o_mask = take(TS * 8);
+  L.o_ival = take(A.ni * TS * 8);
+  L.o_fval = take(A.nf * TS * 8);
+  L.o_mval = take(mm ? TS * 8 : 0);
+  L.o_i32 = take(A.ni * TS * 4);
+  L.o_cnt = take(Lcap * kM * 4);
   L.o_lstate = take(L.LH * 4);
   L.o_lprov = take(Lcap * 4);
   L.o_hist = take(Lcap * 4);
   L.o_offs = take(Lcap * 4);
   L.o_runoffs = take((Lcap + 1) * 4);
+  L.o_ucnt = take((T / 32) * Lcap * 2);
+  L.o_queue = take(T * 4);
   L.o_slot = take(T * 2);
-  L.o_order = take(T * 2);
+  L.o_rank = take(T);
+  L.o_tcs = take(5 * 32 * 8);
   L.o_misc = take(sizeof(Misc));
   L.bytes = off;
   return L;
 }
 
-// Largest tile whose smem holds min(G_cap, 1024) local slots; with fewer slots prefer a
-// smaller tile until at least 64 fit.
+// Local slot capacity: min(G_cap, 256).  Prefer a layout that leaves room for two CTAs
+// per SM; otherwise the largest tile that fits one CTA with at least 64 slots.
 static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, SmemLayout* out) {
-  const int want = (int)std::min<int64_t>(std::max<int64_t>(G_cap, 1), 1024);
+  const int want = (int)std::min<int64_t>(std::max<int64_t>(G_cap, 1), 256);
+  const int half = smem_max / 3 - 2048;
+  for (int T : {1024, 512}) {
+    SmemLayout L = make_layout(A, T, want);
+    if (L.bytes <= half) {
+      *out = L;
+      return true;
+    }
+  }
   for (int T : {2048, 1024, 512}) {
-    int lo = 0, hi = want;  // largest Lcap in [1, want] that fits
+    int lo = 0, hi = want;
     while (lo < hi) {
       int mid = (lo + hi + 1) / 2;
       if (make_layout(A, T, mid).bytes <= smem_max) lo = mid; else hi = mid - 1;
@@ -968,15 +1174,15 @@ static MMLayout mm_layout(int64_t G_cap, int smem_max) {
 
 template <int NI, int NF, int MM>
 static cudaError_t launch_smem(const AggPlan& p, const SmemLayout& L, int sms, cudaStream_t st) {
-  auto k = k_agg_smem<NI, NF, MM>;
+  auto k = k_agg_tiles<NI, NF, MM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, L.bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTileThreads, L.bytes);
   per_sm = std::max(1, per_sm);
   const int64_t tiles = (p.n_rows + L.T - 1) / L.T;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * per_sm));
-  k<<<grid, kThreads, L.bytes, st>>>(p, L);
+  k<<<grid, kTileThreads, L.bytes, st>>>(p, L);
   note_launch();
   return cudaGetLastError();
 }

@@ -24,36 +24,65 @@ __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
   return z;
 }
 
-// pac_hash (§2, §4, R1 + R2 "rejection flips").  `cand` tracks the
-// positions that still hold the majority value; a draw that lands on one flips it.
-__device__ __forceinline__ uint64_t pac_hash_dev(uint64_t key, uint64_t salt) {
-  uint64_t x = fmix64(key ^ salt);
-  int c = __popcll(x);
-  if (c == 32) return x;
-  uint64_t cand = (c > 32) ? x : ~x;
-  int k = (c > 32) ? (c - 32) : (32 - c);
-  uint64_t w = fmix64(x ^ 0xD1B54A32D192ED03ull);
-#pragma unroll 1
-  for (int word = 0; word < 64; ++word) {
+// pac_hash (§2, §4, R1 + R2 "rejection flips").
+// `cand` holds the positions that still carry the majority value; a draw that lands on one
+// flips it (k--).  The final mask is x ^ (cand_initial ^ cand_final).  Draws are processed
+// one 10-draw word at a time, branch-free inside the word (a lane with k == 0 keeps
+// drawing without effect), so a warp diverges only at word granularity.
+constexpr uint64_t kDrawSeed = 0xD1B54A32D192ED03ull;
+constexpr uint64_t kDrawStep = 0x9E3779B97F4A7C15ull;
+
+__device__ __forceinline__ void draw_word(uint64_t w, uint64_t& cand, int& k) {
 #pragma unroll
-    for (int t = 0; t < 10; ++t) {
-      uint32_t p = (uint32_t)(w >> (6 * t)) & 63u;
-      uint64_t bit = 1ull << p;
-      if (cand & bit) {
-        cand ^= bit;
-        x ^= bit;
-        if (--k == 0) return x;
-      }
-    }
-    w = fmix64(w + 0x9E3779B97F4A7C15ull);
+  for (int t = 0; t < 10; ++t) {
+    const uint32_t p = (uint32_t)(w >> (6 * t)) & 63u;
+    uint64_t hit = cand & (1ull << p);
+    hit = (k > 0) ? hit : 0ull;
+    cand ^= hit;
+    k -= (hit != 0ull) ? 1 : 0;
+  }
+}
+
+struct HashState {
+  uint64_t x;     // fmix64(key ^ salt)
+  uint64_t cand;  // current majority positions
+  int k;          // flips still needed
+};
+
+// mix + popcount + the first draw word.  Returns the state after word 0.
+__device__ __forceinline__ HashState pac_hash_begin(uint64_t key, uint64_t salt) {
+  HashState h;
+  h.x = fmix64(key ^ salt);
+  const int c = __popcll(h.x);
+  h.k = (c > 32) ? (c - 32) : (32 - c);
+  h.cand = (c > 32) ? h.x : ~h.x;
+  if (h.k > 0) draw_word(fmix64(h.x ^ kDrawSeed), h.cand, h.k);
+  return h;
+}
+
+// Continues from word 1 until k == 0 (or the R2 safety net).  `mask_now` is the mask
+// after word 0, i.e. x ^ (cand_initial ^ cand).
+__device__ __forceinline__ uint64_t pac_hash_finish(uint64_t x, uint64_t cand, int k) {
+  const uint64_t cand0 = (__popcll(x) > 32) ? x : ~x;
+  uint64_t w = fmix64(x ^ kDrawSeed);
+#pragma unroll 1
+  for (int word = 1; word < 64 && k > 0; ++word) {
+    w = fmix64(w + kDrawStep);
+    draw_word(w, cand, k);
   }
   while (k > 0) {  // safety net of R2 (never reached in practice)
-    uint64_t low = cand & (~cand + 1ull);
+    const uint64_t low = cand & (~cand + 1ull);
     cand ^= low;
-    x ^= low;
     --k;
   }
-  return x;
+  return x ^ (cand0 ^ cand);
+}
+
+__device__ __forceinline__ uint64_t pac_hash_dev(uint64_t key, uint64_t salt) {
+  HashState h = pac_hash_begin(key, salt);
+  const uint64_t cand0 = (__popcll(h.x) > 32) ? h.x : ~h.x;
+  if (h.k == 0) return h.x ^ (cand0 ^ h.cand);
+  return pac_hash_finish(h.x, h.cand, h.k);
 }
 
 // ------------------------------------------------------------------ Philox4x32-10 (R13)
