@@ -75,7 +75,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -161,7 +161,7 @@ def run_reference(args, w):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--rows", type=int, default=0, help="override rows per GPU (testing only)")
@@ -251,24 +251,27 @@ def main():
     value = (n * world) / (ms_step / 1e3)
 
     # ---- end-to-end through the public API: pinned host inputs H2D + releases D2H
-    host = {"pu": cols["pu"].cpu().pin_memory(), "keys": [k.cpu().pin_memory() for k in keys],
-            "vals": [None if v is None else v.cpu().pin_memory() for v in vals]}
-    h2d = host["pu"].numel() * 8 + sum(k.numel() * k.element_size() for k in host["keys"]) + sum(
-        v.numel() * v.element_size() for v in host["vals"] if v is not None)
+    host = {"pu": cols["pu"].cpu().pin_memory(), "keys": [k.cpu().pin_memory() for k in keys]}
     d2h = G * len(kinds) * 9  # releases (f64) + NULL flags (u8)
     res_host = torch.empty(G_cap, len(kinds), dtype=torch.float64).pin_memory()
     null_host = torch.empty(G_cap, len(kinds), dtype=torch.uint8).pin_memory()
     d_pu = torch.empty_like(cols["pu"])
     d_keys = [torch.empty_like(k) for k in keys]
-    d_vals = [None if v is None else torch.empty_like(v) for v in vals]
+    # one device buffer per distinct column (aggregates may share a column, e.g. MIN+MAX)
+    uniq = {}
+    for v in vals:
+        if v is not None and id(v) not in uniq:
+            uniq[id(v)] = (torch.empty_like(v), v.cpu().pin_memory())
+    d_vals = [None if v is None else uniq[id(v)][0] for v in vals]
+    h2d = host["pu"].numel() * 8 + sum(k.numel() * k.element_size() for k in host["keys"]) + sum(
+        h.numel() * h.element_size() for _, h in uniq.values())
 
     def e2e_step():
         d_pu.copy_(host["pu"], non_blocking=True)
         for d, h in zip(d_keys, host["keys"]):
             d.copy_(h, non_blocking=True)
-        for d, h in zip(d_vals, host["vals"]):
-            if d is not None:
-                d.copy_(h, non_blocking=True)
+        for d, h in uniq.values():
+            d.copy_(h, non_blocking=True)
         t = step(d_pu, d_keys, d_vals)
         res_host.copy_(fin.release, non_blocking=True)
         null_host.copy_(fin.is_null, non_blocking=True)

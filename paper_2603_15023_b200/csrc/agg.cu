@@ -15,6 +15,7 @@
 //               into the caller's table; K re-derived from counts / extremes.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -44,6 +45,7 @@ struct AggPlan {
   uint32_t hmask;
   int* gcounter;
   unsigned long long* gmaxabs;  // max |v| over int64 sum columns (overflow check)
+  unsigned long long* dbg;      // [0] rows sent to the HBM tier, [1] max local slots used
   int64_t G_cap;
   unsigned long long* prov_key;
   unsigned long long* prov_rows;
@@ -117,16 +119,22 @@ __device__ int global_slot(const AggPlan& p, uint64_t key) {
 
 // CTA-local dictionary: code = s+1 for local slot s (< Lcap); kOvfBase + prov + 1 for a
 // key that has no local slot (its rows go straight to the HBM table; prov -1 = dropped).
+// An empty entry is claimed with CAS first; only then is the entry counted, so concurrent
+// contenders for one key never inflate the fill count.  At half full no more keys are
+// inserted (their rows use the HBM dictionary directly).
 __device__ int local_code(const AggPlan& p, uint64_t key, unsigned long long* lkey, int* lstate,
                           int LH, int* lprov, int Lcap, Misc* misc) {
   uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 40) & (LH - 1);
   for (;;) {
     int st = *(volatile int*)&lstate[h];
     if (st == 0) {
-      if (atomicAdd(&misc->ndict, 1) >= LH / 2) {  // dictionary full: no insert
-        return kOvfBase + global_slot(p, key) + 1;
-      }
       if (atomicCAS(&lstate[h], 0, -1) == 0) {
+        if (atomicAdd(&misc->ndict, 1) >= LH / 2) {  // too full: release, use the HBM tier
+          atomicSub(&misc->ndict, 1);
+          __threadfence_block();
+          atomicExch(&lstate[h], 0);
+          return kOvfBase + global_slot(p, key) + 1;
+        }
         lkey[h] = key;
         int s = atomicAdd(&misc->nlocal, 1);
         int prov = global_slot(p, key);
@@ -141,7 +149,6 @@ __device__ int local_code(const AggPlan& p, uint64_t key, unsigned long long* lk
         atomicExch(&lstate[h], code);
         return code;
       }
-      atomicSub(&misc->ndict, 1);
       continue;
     }
     if (st < 0) continue;
@@ -169,6 +176,7 @@ template <int NI, int NF, int MM>
 __device__ __forceinline__ void global_row_update(const AggPlan& p, int prov, uint64_t m,
                                                   const long long (&iv)[NI > 0 ? NI : 1],
                                                   const double (&fv)[NF > 0 ? NF : 1], double mv) {
+  atomicAdd(&p.dbg[0], 1ull);
   if (prov < 0) return;
   atomicAdd(&p.prov_rows[prov], 1ull);
   const size_t b = (size_t)prov * kM;
@@ -626,6 +634,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
 
   // ---------------- CTA table -> provisional HBM table
   const int nloc = min(misc->nlocal, Lcap);
+  if (tid == 0) atomicMax(&p.dbg[1], (unsigned long long)misc->nlocal);
   for (int i = tid; i < nloc * kM; i += nth) {
     const int s = i / kM;
     const int prov = lprov[s];
@@ -989,7 +998,10 @@ struct AccSet {
   int src_idx[PAC_MAX_AGGS];
 };
 
-static int build_accs(const pac_agg_spec* aggs, int n_aggs, AccSet* A, bool allow_null = false) {
+// Accumulator set of a call.  kinds_only: value pointers are ignored (NULL allowed, no
+// column-identity rules) -- for the entry points that only need the aggregate kinds.
+static int build_accs(const pac_agg_spec* aggs, int n_aggs, AccSet* A, bool allow_null = false,
+                      bool kinds_only = false) {
   if (n_aggs < 1 || n_aggs > PAC_MAX_AGGS || !aggs) return PAC_E_INVAL;
   bool only_mm = true;
   for (int a = 0; a < n_aggs; ++a) {
@@ -1022,7 +1034,7 @@ static int build_accs(const pac_agg_spec* aggs, int n_aggs, AccSet* A, bool allo
       A->src_kind[a] = 2;
       A->src_idx[a] = f;
     } else {
-      if (A->mcol && A->mcol != v) return PAC_E_INVAL;
+      if (!kinds_only && A->mcol && A->mcol != v) return PAC_E_INVAL;
       A->mcol = v;
       if (k == PAC_MIN_F64) {
         A->has_min = 1;
@@ -1119,30 +1131,33 @@ static SmemLayout make_layout(const AccSet& A, int T, int Lcap) {
   return L;
 }
 
-// Local slot capacity: min(G_cap, 256).  Prefer a layout that leaves room for two CTAs
-// per SM; otherwise the largest tile that fits one CTA with at least 64 slots.
+// Local slot capacity: min(G_cap, 256).  Prefer a layout that leaves room for three CTAs
+// per SM; otherwise one or two CTAs with as many slots as fit (tile 1024, else 512).
 static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, SmemLayout* out) {
   const int want = (int)std::min<int64_t>(std::max<int64_t>(G_cap, 1), 256);
-  const int half = smem_max / 3 - 2048;
+  const int third = smem_max / 3 - 2048;
   for (int T : {1024, 512}) {
     SmemLayout L = make_layout(A, T, want);
-    if (L.bytes <= half) {
+    if (L.bytes <= third) {
       *out = L;
       return true;
     }
   }
-  for (int T : {2048, 1024, 512}) {
+  int best = 0, bestT = 0;
+  for (int T : {1024, 512}) {
     int lo = 0, hi = want;
     while (lo < hi) {
       int mid = (lo + hi + 1) / 2;
       if (make_layout(A, T, mid).bytes <= smem_max) lo = mid; else hi = mid - 1;
     }
-    if (lo < 1) continue;
-    if (lo < want && lo < 64 && T > 512) continue;
-    *out = make_layout(A, T, lo);
-    return true;
+    if (lo > best) {
+      best = lo;
+      bestT = T;
+    }
   }
-  return false;
+  if (best < 1) return false;
+  *out = make_layout(A, bestT, best);
+  return true;
 }
 
 static MMLayout mm_layout(int64_t G_cap, int smem_max) {
@@ -1294,6 +1309,7 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
   p.gcounter = (int*)(ws + W.o_ctr);
   int* Gdev = (int*)(ws + W.o_ctr + 4);
   p.gmaxabs = (unsigned long long*)(ws + W.o_ctr + 8);
+  p.dbg = (unsigned long long*)(ws + W.o_ctr + 16);
   p.G_cap = G_cap;
   p.prov_key = (unsigned long long*)(ws + W.o_pkey);
   p.prov_rows = (unsigned long long*)(ws + W.o_prows);
@@ -1336,6 +1352,9 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
     } else {
       SmemLayout L{};
       if (!choose_layout(A, G_cap, smem_max, &L)) return PAC_E_INVAL;
+      if (getenv("PAC_DEBUG"))
+        fprintf(stderr, "[libpac] k_agg_tiles<%d,%d,%d> T=%d Lcap=%d LH=%d smem=%d B (G_cap=%lld)\n", A.ni,
+                A.nf, (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0), L.T, L.Lcap, L.LH, L.bytes, (long long)G_cap);
       const int mm = (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0);
       profile_begin(st);
       e = kLaunch[A.ni][A.nf][mm](p, L, sms, st);
@@ -1372,6 +1391,12 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
     int blocks = (int)std::min<int64_t>((G_cap + 7) / 8, (int64_t)sms * 16);
     k_gather<<<std::max(1, blocks), 256, 0, st>>>(p, Gdev, perm, *out, n_aggs, meta, meta + PAC_MAX_AGGS);
     note_launch();
+  }
+  if (getenv("PAC_DEBUG")) {
+    unsigned long long d[2] = {0, 0};
+    cudaMemcpyAsync(d, p.dbg, 16, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[libpac] HBM-tier rows %llu, max local slots used %llu\n", d[0], d[1]);
   }
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
@@ -1454,7 +1479,7 @@ extern "C" int pac_table_rederive_presence(const pac_table* t, const pac_agg_spe
                                            int64_t G_cap, pac_stream_t stream) {
   AccSet A;
   if (!t || G_cap < 1) return PAC_E_INVAL;
-  int rc = build_accs(aggs, n_aggs, &A);
+  int rc = build_accs(aggs, n_aggs, &A, true, true);  // only the kinds matter here
   if (rc) return rc;
   int mm_a = -1, mm_kind = 0;
   for (int a = 0; a < n_aggs; ++a)
@@ -1475,7 +1500,7 @@ extern "C" int pac_table_remap(const pac_table* in, const uint64_t* d_union_keys
                                pac_stream_t stream) {
   AccSet A;
   if (!in || !out || !d_union_keys || G_union < 1 || G_cap_in < 1) return PAC_E_INVAL;
-  int rc = build_accs(aggs, n_aggs, &A);
+  int rc = build_accs(aggs, n_aggs, &A, true, true);  // only the kinds matter here
   if (rc) return rc;
   // kinds are passed by value through a small device buffer embedded in the launch
   static int* d_kinds = nullptr;

@@ -1,0 +1,125 @@
+"""Multi-process (world_size 2, gloo, CPU) test of the row-sharded merge plumbing
+(paper analogue: thread-local partial aggregates + combine).
+
+Each rank builds the partial 64-world table of its contiguous row shard (the oracle stands
+in for the per-GPU kernel here), then the product's torch.distributed plumbing --
+union dictionary, all_reduce ops per array -- merges them.  The merged table must equal
+the unsharded table exactly (integers, MIN/MAX) or to 1e-12 (f64 sums)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import datagen as dg
+
+KINDS = [dg.AGG_COUNT, dg.AGG_SUM_I64, dg.AGG_AVG_F64, dg.AGG_MIN_F64, dg.AGG_MAX_F64]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _case(n=40_000, seed=3):
+    rng = np.random.default_rng(seed)
+    pu = rng.integers(0, 3000, n).astype(np.int64)
+    g = rng.integers(0, 40, n).astype(np.int32)
+    iv = rng.integers(-10**6, 10**6, n).astype(np.int64)
+    fv = rng.normal(5, 2, n)
+    return pu, g, iv, fv
+
+
+def _aggs(iv, fv):
+    vals = {dg.AGG_COUNT: None, dg.AGG_SUM_I64: iv, dg.AGG_AVG_F64: fv, dg.AGG_MIN_F64: fv,
+            dg.AGG_MAX_F64: fv}
+    return [(k, vals[k]) for k in KINDS]
+
+
+def _worker(rank, world, port, q):
+    try:
+        import oracle
+        from paper_2603_15023_b200 import dist as pdist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        pu, g, iv, fv = _case()
+        n = len(pu)
+        lo, hi = rank * n // world, (rank + 1) * n // world
+        # rank 1 drops a group entirely so the union dictionary differs from the local one
+        sel = np.arange(lo, hi)
+        if rank == 1:
+            sel = sel[g[sel] != 7]
+        masks = oracle.pac_hash(pu[sel], 99)
+        part = oracle.agg(masks, [g[sel]], _aggs(iv[sel], fv[sel]))
+        local_keys = torch.from_numpy(part["keys"].view(np.int64).copy())
+        union, same = pdist.union_keys(local_keys)
+        assert not same
+        ukeys = union.numpy().view(np.uint64)
+        # lay the partial table out on the union dictionary (the device does this with
+        # pac_table_remap; here plain numpy on the oracle's arrays)
+        G = len(ukeys)
+        idx = np.searchsorted(ukeys, part["keys"])
+        rows = torch.zeros(G, dtype=torch.int64)
+        count = torch.zeros(G, 64, dtype=torch.int64)
+        worlds = []
+        rows[idx] = torch.from_numpy(part["rows"])
+        count[idx] = torch.from_numpy(part["count"])
+        for a, k in enumerate(KINDS):
+            if k == dg.AGG_COUNT:
+                worlds.append(None)
+                continue
+            fill = {dg.AGG_MIN_F64: np.inf, dg.AGG_MAX_F64: -np.inf}.get(k, 0)
+            dt = torch.int64 if k == dg.AGG_SUM_I64 else torch.float64
+            w = torch.full((G, 64), fill, dtype=dt)
+            w[idx] = torch.from_numpy(part["world"][a])
+            worlds.append(w)
+        pdist.allreduce_table_tensors(rows, count, worlds, KINDS)
+        q.put((rank, ukeys, rows.numpy(), count.numpy(), [None if w is None else w.numpy() for w in worlds]))
+        dist.destroy_process_group()
+    except Exception as e:  # surface the failure to the parent
+        q.put((rank, "error", repr(e)))
+
+
+def test_row_sharded_merge_equals_unsharded_table(orc):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for o in out:
+        assert not (isinstance(o[1], str) and o[1] == "error"), o
+    pu, g, iv, fv = _case()
+    n = len(pu)
+    keep = np.ones(n, dtype=bool)
+    keep[n // 2:] &= g[n // 2:] != 7   # the rows rank 1 left out
+    pu, g, iv, fv = pu[keep], g[keep], iv[keep], fv[keep]
+    ref = orc.agg(orc.pac_hash(pu, 99), [g], _aggs(iv, fv))
+    for rank, ukeys, rows, count, worlds in out:
+        np.testing.assert_array_equal(ukeys, ref["keys"])
+        np.testing.assert_array_equal(rows, ref["rows"])
+        np.testing.assert_array_equal(count, ref["count"])
+        # K re-derived from the merged counts (NCCL has no OR reduction) equals the OR
+        K = np.array([sum(1 << j for j in range(64) if c[j] > 0) for c in count], dtype=np.uint64)
+        np.testing.assert_array_equal(K, ref["K"])
+        for a, k in enumerate(KINDS):
+            if k == dg.AGG_COUNT:
+                continue
+            if k == dg.AGG_AVG_F64:
+                np.testing.assert_allclose(worlds[a], ref["world"][a], rtol=1e-12)
+            else:
+                np.testing.assert_array_equal(worlds[a], ref["world"][a])
+
+
+def test_reduce_ops_follow_aggregate_kind():
+    from paper_2603_15023_b200 import dist as pdist
+    assert pdist.reduce_ops_for(KINDS) == ["none", "sum", "sum", "min", "max"]

@@ -221,3 +221,48 @@ def test_null_and_zero_variance_edge_cells(orc):
     G = ref["G"]
     assert_releases_close(rel[:G].cpu().numpy(), r_o, d_o, isn[:G].cpu().numpy(), n_o)
     np.testing.assert_allclose(s.query()["P"], P, atol=1e-12)
+
+
+# ------------------------------------------------------------------ merge kernels (a5, e)
+def test_shard_remap_merge_rederive_matches_unsharded(orc):
+    """Two row shards aggregated separately, laid out on the union dictionary with
+    pac_table_remap, summed / min-maxed (what the NCCL allreduce does across GPUs), then K
+    re-derived with pac_table_rederive_presence: equals the unsharded oracle table."""
+    rng = np.random.default_rng(12)
+    n = 120_000
+    pu = rng.integers(0, 9000, n).astype(np.int64)
+    g = rng.integers(0, 300, n).astype(np.int32)
+    g[n // 2:][g[n // 2:] == 5] = 6          # shard 1 lacks group 5
+    iv = rng.integers(-10**9, 10**9, n).astype(np.int64)
+    fv = rng.normal(0, 10, n)
+    for kinds in ([dg.AGG_COUNT, dg.AGG_SUM_I64, dg.AGG_AVG_F64], [dg.AGG_MIN_F64, dg.AGG_MAX_F64]):
+        vals = {dg.AGG_COUNT: None, dg.AGG_SUM_I64: iv, dg.AGG_AVG_F64: fv, dg.AGG_MIN_F64: fv,
+                dg.AGG_MAX_F64: fv}
+        parts = []
+        for lo, hi in ((0, n // 2), (n // 2, n)):
+            shard = {id(iv): iv[lo:hi].copy(), id(fv): fv[lo:hi].copy()}  # one copy per column
+            aggs = [(k, None if vals[k] is None else shard[id(vals[k])]) for k in kinds]
+            t, _ = run_gpu(aggs, [g[lo:hi].copy()], pu=pu[lo:hi].copy(), salt=77, G_cap=512)
+            t.check()
+            parts.append((t, aggs))
+        keys = np.union1d(pac.as_u64(parts[0][0].group_key[:parts[0][0].check()]),
+                          pac.as_u64(parts[1][0].group_key[:parts[1][0].check()]))
+        ukeys = to_dev(keys.view(np.int64))
+        mapped = [pac.remap(t, ukeys, [(k, to_dev(v) if v is not None else None) for k, v in aggs])
+                  for t, aggs in parts]
+        a, b = mapped
+        a.rows += b.rows
+        if a.count is not None:
+            a.count += b.count
+        for i, k in enumerate(kinds):
+            if k in (dg.AGG_SUM_I64, dg.AGG_AVG_F64):
+                a.world[i] += b.world[i]
+            elif k == dg.AGG_MIN_F64:
+                torch.minimum(a.world[i], b.world[i], out=a.world[i])
+            elif k == dg.AGG_MAX_F64:
+                torch.maximum(a.world[i], b.world[i], out=a.world[i])
+        a.presence.zero_()
+        pac.rederive_presence(a, [(k, None) for k in kinds])
+        full_aggs = [(k, vals[k]) for k in kinds]
+        ref = orc.agg(orc.pac_hash(pu, 77), [g], full_aggs)
+        assert_tables_equal(a.to_host(), ref)
