@@ -308,7 +308,7 @@ def main():
                        "description": w.description},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(w.name),
-                         "kernel": "k_agg_smem (pac_agg_grouped main kernel)",
+                         "kernel": "k_agg_tiles (pac_agg_grouped main kernel)",
                          "kernel_ms": k_avg_ms, "kernel_share_of_step": k_avg_ms / ms_step,
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": alg_bytes},
