@@ -46,6 +46,13 @@ struct AggPlan {
   int* gcounter;
   unsigned long long* gmaxabs;  // max |v| over int64 sum columns (overflow check)
   unsigned long long* dbg;      // [0] rows sent to the HBM tier, [1] max local slots used
+  // raw input columns staged per tile by 1-D TMA bulk copies (k_agg_tiles):
+  // 0 = pu_key or mask, 1..n_keys = key columns, then int64 sums, f64 sums, min/max column
+  int nraw, tma_ok;
+  const void* raw_src[1 + PAC_MAX_KEYS + 5];
+  int raw_eb[1 + PAC_MAX_KEYS + 5];
+  int raw_off[1 + PAC_MAX_KEYS + 5];  // byte offset of the column inside the raw tile buffer
+  int raw_bytes;                       // bytes of one staged tile
   int64_t G_cap;
   unsigned long long* prov_key;
   unsigned long long* prov_rows;
@@ -60,7 +67,7 @@ struct SmemLayout {
   int T, TS, Lcap, LH;
   int o_lkey, o_lstate, o_lprov, o_lrows, o_cnt, o_isum, o_fsum, o_min, o_max;
   int o_mask, o_slot, o_rank, o_ucnt, o_queue, o_ival, o_i32, o_fval, o_mval, o_hist, o_offs,
-      o_runoffs, o_tcs, o_misc;
+      o_runoffs, o_tcs, o_raw, o_mbar, o_misc;
   int bytes;
 };
 
@@ -201,6 +208,70 @@ __global__ void __launch_bounds__(256) k_mask(const long long* __restrict__ key,
     out[i] = pac_hash_dev((uint64_t)__ldg(key + i), salt);
 }
 
+// ------------------------------------------------------------------ TMA bulk staging
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* m, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(m)), "r"(parity) : "memory");
+}
+// one thread: stage the raw columns of the full tile starting at row `base`
+__device__ __forceinline__ void issue_tile(const AggPlan& p, unsigned char* raw, unsigned long long* mbar,
+                                           int64_t base, int T) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(mbar, (uint32_t)p.raw_bytes);
+  for (int i = 0; i < p.nraw; ++i)
+    bulk_g2s(raw + p.raw_off[i], (const char*)p.raw_src[i] + base * p.raw_eb[i], (uint32_t)(T * p.raw_eb[i]), mbar);
+}
+
+// Row accessors: staged tiles read the raw smem copy, other tiles read global memory.
+struct RawTile {
+  const unsigned char* raw;
+  bool staged;
+};
+__device__ __forceinline__ uint64_t raw_u64(const AggPlan& p, const RawTile& t, int col, const void* g,
+                                            int64_t r, int li) {
+  return t.staged ? ((const unsigned long long*)(t.raw + p.raw_off[col]))[li]
+                  : (uint64_t)__ldg((const unsigned long long*)g + r);
+}
+__device__ __forceinline__ uint64_t raw_group_key(const AggPlan& p, const RawTile& t, int64_t r, int li) {
+  uint64_t packed = 0;
+#pragma unroll
+  for (int c = 0; c < PAC_MAX_KEYS; ++c) {
+    if (c < p.n_keys) {
+      const int w = p.key_bytes[c];
+      uint64_t v;
+      if (t.staged) {
+        const unsigned char* col = t.raw + p.raw_off[1 + c];
+        if (w == 1) v = col[li];
+        else if (w == 2) v = ((const unsigned short*)col)[li];
+        else if (w == 4) v = ((const unsigned*)col)[li];
+        else v = ((const unsigned long long*)col)[li];
+        v ^= 1ull << (8 * w - 1);
+      } else {
+        v = load_key_part(p.key_col[c], w, r);
+      }
+      packed = (w == 8) ? v : ((packed << (8 * w)) | v);
+    }
+  }
+  return packed;
+}
+
 // ------------------------------------------------------------------ k_agg_tiles (v3)
 // Bit-matrix transpose of a 32-row run: on input lane r holds row r's
 // 32-bit mask word; on output lane c holds the pattern of world c over the run.  Stage s
@@ -241,6 +312,193 @@ __device__ __forceinline__ bool finite_bits(double v) {
   return (__double2hiint(v) & 0x7FF00000) != 0x7FF00000;
 }
 
+// Register accumulators of the slot a warp is currently working on (lane: worlds lane, lane+32).
+template <int NI, int NF, int MM>
+struct WarpAcc {
+  int cur;
+  unsigned c0, c1;
+  long long ia0[NI > 0 ? NI : 1], ia1[NI > 0 ? NI : 1];
+  double fa0[NF > 0 ? NF : 1], fa1[NF > 0 ? NF : 1];
+  double mn0, mn1, mx0, mx1;
+
+  __device__ __forceinline__ void reset() {
+    c0 = c1 = 0;
+#pragma unroll
+    for (int c = 0; c < NI; ++c) ia0[c] = ia1[c] = 0;
+#pragma unroll
+    for (int c = 0; c < NF; ++c) fa0[c] = fa1[c] = 0.0;
+    mn0 = mn1 = INFINITY;
+    mx0 = mx1 = -INFINITY;
+  }
+  // add into the CTA's smem table (shared by the warps working on the same slot)
+  __device__ __forceinline__ void flush(unsigned* cnt, unsigned long long* isum, double* fsum, long long* emin,
+                                        long long* emax, int Lcap, int lane) {
+    if (cur < 0) return;
+    const size_t b = (size_t)cur * kM;
+    if (c0) atomicAdd(&cnt[b + lane], c0);
+    if (c1) atomicAdd(&cnt[b + lane + 32], c1);
+#pragma unroll
+    for (int c = 0; c < NI; ++c) {
+      atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane], (unsigned long long)ia0[c]);
+      atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane + 32], (unsigned long long)ia1[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NF; ++c) {
+      atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane], fa0[c]);
+      atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane + 32], fa1[c]);
+    }
+    if (MM & 1) {
+      atomicMin(&emin[b + lane], enc_f64(mn0));
+      atomicMin(&emin[b + lane + 32], enc_f64(mn1));
+    }
+    if (MM & 2) {
+      atomicMax(&emax[b + lane], enc_f64(mx0));
+      atomicMax(&emax[b + lane + 32], enc_f64(mx1));
+    }
+    reset();
+  }
+};
+
+struct RunCtx {  // read-only per-tile state of phase C
+  const unsigned long long* smask;
+  const long long* sival;
+  const int* si32;
+  const double* sfval;
+  const double* smval;
+  const int* hist;
+  const int* offs;
+  const int* runoffs;
+  const uint2* tcs;
+  int TS, Lcap, R;
+};
+
+// Phase C of one tile for one warp: runs [r0, r1) of the tile's slot-sorted rows.
+// SMALL: int64 values of the tile fit int32 nibble tables; FIN: f64 values are finite, so
+// the f64 nibble tables are built with exact 0/1 FMAs.
+template <int NI, int NF, int MM, bool SMALL, bool FIN>
+__device__ __forceinline__ void run_tiles(WarpAcc<NI, NF, MM>& acc, const RunCtx& x, unsigned* cnt,
+                                          unsigned long long* isum, double* fsum, long long* emin,
+                                          long long* emax, int wid, int nw, int lane) {
+  const int R = x.R, TS = x.TS;
+  const int r0 = (int)(((long long)R * wid) / nw);
+  const int r1 = (int)(((long long)R * (wid + 1)) / nw);
+  if (r0 >= r1) return;
+  const int sub = lane & 15;
+  const int tsrc = (lane >> 4) << 2;
+  const int ib0 = sub & 1, ib1 = (sub >> 1) & 1, ib2 = (sub >> 2) & 1, ib3 = (sub >> 3) & 1;
+  const double db0 = ib0, db1 = ib1, db2 = ib2, db3 = ib3;
+  int s;
+  {
+    int lo = 0, hi = x.Lcap;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (x.runoffs[mid] <= r0) lo = mid; else hi = mid - 1;
+    }
+    s = lo;
+  }
+  int rs_end = x.runoffs[s + 1];
+  int k0 = 32 * (r0 - x.runoffs[s]);
+  int slot_beg = x.offs[s], slot_len = x.hist[s];
+  for (int r = r0; r < r1; ++r) {
+    if (r >= rs_end) {  // next non-empty slot
+      do {
+        ++s;
+        rs_end = x.runoffs[s + 1];
+      } while (rs_end <= r);
+      k0 = 0;
+      slot_beg = x.offs[s];
+      slot_len = x.hist[s];
+    }
+    if (s != acc.cur) {
+      acc.flush(cnt, isum, fsum, emin, emax, x.Lcap, lane);
+      acc.cur = s;
+    }
+    const int beg = slot_beg + k0;
+    const int len = min(32, slot_len - k0);
+    k0 += 32;
+    const uint64_t m = lane < len ? x.smask[beg + lane] : 0ull;
+    uint32_t P = (uint32_t)m, Q = (uint32_t)(m >> 32);
+    transpose2x32(P, Q, x.tcs, lane);
+    acc.c0 += __popc(P);
+    acc.c1 += __popc(Q);
+    // nibble indices: table A (lanes 0-15) covers rows 8q..8q+3, B (16-31) rows 8q+4..8q+7;
+    // shfl uses only the low 5 bits of the source lane.
+    const uint32_t PA = P & 0x0F0F0F0Fu, PB = ((P >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
+    const uint32_t QA = Q & 0x0F0F0F0Fu, QB = ((Q >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
+    const int nq = (len + 7) >> 3;
+    int rs0[NI > 0 ? NI : 1], rs1[NI > 0 ? NI : 1];
+#pragma unroll
+    for (int c = 0; c < NI; ++c) rs0[c] = rs1[c] = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q >= nq) break;
+      const int a0 = (int)(PA >> (8 * q)), b0 = (int)(PB >> (8 * q));
+      const int a1 = (int)(QA >> (8 * q)), b1 = (int)(QB >> (8 * q));
+      const int row = beg + 8 * q + tsrc;
+#pragma unroll
+      for (int c = 0; c < NI; ++c) {
+        if (SMALL) {
+          const int4 v = *(const int4*)(x.si32 + c * TS + row);
+          const int t = v.x * ib0 + v.y * ib1 + v.z * ib2 + v.w * ib3;
+          rs0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
+          rs1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
+        } else {
+          const longlong2 u = *(const longlong2*)(x.sival + c * TS + row);
+          const longlong2 w = *(const longlong2*)(x.sival + c * TS + row + 2);
+          const long long t = u.x * ib0 + u.y * ib1 + w.x * ib2 + w.y * ib3;
+          acc.ia0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
+          acc.ia1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NF; ++c) {
+        const double2 u = *(const double2*)(x.sfval + c * TS + row);
+        const double2 w = *(const double2*)(x.sfval + c * TS + row + 2);
+        double t;
+        if (FIN) {  // exact: 0*v + t == t and 1*v + t == v + t for finite v
+          t = fma(db3, w.y, fma(db2, w.x, fma(db1, u.y, db0 * u.x)));
+        } else {
+          t = ib0 ? u.x : 0.0;
+          if (ib1) t += u.y;
+          if (ib2) t += w.x;
+          if (ib3) t += w.y;
+        }
+        acc.fa0[c] += shfl_d(t, a0);
+        acc.fa0[c] += shfl_d(t, b0);
+        acc.fa1[c] += shfl_d(t, a1);
+        acc.fa1[c] += shfl_d(t, b1);
+      }
+      if (MM) {
+        const double2 u = *(const double2*)(x.smval + row);
+        const double2 w = *(const double2*)(x.smval + row + 2);
+        if (MM & 1) {
+          double t = ib0 ? u.x : INFINITY;
+          if (ib1) t = fmin(t, u.y);
+          if (ib2) t = fmin(t, w.x);
+          if (ib3) t = fmin(t, w.y);
+          acc.mn0 = fmin(acc.mn0, fmin(shfl_d(t, a0), shfl_d(t, b0)));
+          acc.mn1 = fmin(acc.mn1, fmin(shfl_d(t, a1), shfl_d(t, b1)));
+        }
+        if (MM & 2) {
+          double t = ib0 ? u.x : -INFINITY;
+          if (ib1) t = fmax(t, u.y);
+          if (ib2) t = fmax(t, w.x);
+          if (ib3) t = fmax(t, w.y);
+          acc.mx0 = fmax(acc.mx0, fmax(shfl_d(t, a0), shfl_d(t, b0)));
+          acc.mx1 = fmax(acc.mx1, fmax(shfl_d(t, a1), shfl_d(t, b1)));
+        }
+      }
+    }
+    if (SMALL) {
+#pragma unroll
+      for (int c = 0; c < NI; ++c) {
+        acc.ia0[c] += rs0[c];
+        acc.ia1[c] += rs1[c];
+      }
+    }
+  }
+}
+
 template <int NI, int NF, int MM>
 __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLayout L) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -267,6 +525,8 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
   int* offs = (int*)(smem + L.o_offs);
   int* runoffs = (int*)(smem + L.o_runoffs);
   Misc* misc = (Misc*)(smem + L.o_misc);
+  unsigned char* raw = smem + L.o_raw;
+  unsigned long long* mbar = (unsigned long long*)(smem + L.o_mbar);
 
   const int tid = threadIdx.x, nth = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
@@ -297,6 +557,13 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
   const int64_t t_per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * t_per;
   const int64_t t1 = min(ntiles, t0 + t_per);
+  // a tile is staged by TMA when it is full and every column is 16-byte aligned
+  auto staged_tile = [&](int64_t t) { return p.tma_ok && t < t1 && (t + 1) * T <= p.n_rows; };
+  uint32_t phase = 0;
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    if (staged_tile(t0)) issue_tile(p, raw, mbar, t0 * T, T);
+  }
 
   // run-processing state of this warp (lane: worlds lane and lane+32)
   uint2* tcs = (uint2*)(smem + L.o_tcs);
@@ -304,48 +571,9 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
 #pragma unroll
     for (int i = 0; i < 5; ++i) tcs[i * 32 + tid] = transpose_const(tid, i);
   }
-  const int sub = lane & 15;          // subset of this lane's 16-entry table
-  const int tsrc = (lane >> 4) << 2;  // lanes 0-15: rows 8q..8q+3; lanes 16-31: rows 8q+4..8q+7
-  const int ib0 = sub & 1, ib1 = (sub >> 1) & 1, ib2 = (sub >> 2) & 1, ib3 = (sub >> 3) & 1;
-  int cur = -1;
-  unsigned c0 = 0, c1 = 0;
-  long long ia0[NI > 0 ? NI : 1], ia1[NI > 0 ? NI : 1];
-  double fa0[NF > 0 ? NF : 1], fa1[NF > 0 ? NF : 1];
-  double mn0 = INFINITY, mn1 = INFINITY, mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-  for (int c = 0; c < NI; ++c) ia0[c] = ia1[c] = 0;
-#pragma unroll
-  for (int c = 0; c < NF; ++c) fa0[c] = fa1[c] = 0.0;
-
-  auto flush = [&]() {
-    if (cur < 0) return;
-    const size_t b = (size_t)cur * kM;
-    if (c0) atomicAdd(&cnt[b + lane], c0);
-    if (c1) atomicAdd(&cnt[b + lane + 32], c1);
-#pragma unroll
-    for (int c = 0; c < NI; ++c) {
-      atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane], (unsigned long long)ia0[c]);
-      atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane + 32], (unsigned long long)ia1[c]);
-      ia0[c] = ia1[c] = 0;
-    }
-#pragma unroll
-    for (int c = 0; c < NF; ++c) {
-      atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane], fa0[c]);
-      atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane + 32], fa1[c]);
-      fa0[c] = fa1[c] = 0.0;
-    }
-    if (MM & 1) {
-      atomicMin(&emin[b + lane], enc_f64(mn0));
-      atomicMin(&emin[b + lane + 32], enc_f64(mn1));
-    }
-    if (MM & 2) {
-      atomicMax(&emax[b + lane], enc_f64(mx0));
-      atomicMax(&emax[b + lane + 32], enc_f64(mx1));
-    }
-    c0 = c1 = 0;
-    mn0 = mn1 = INFINITY;
-    mx0 = mx1 = -INFINITY;
-  };
+  WarpAcc<NI, NF, MM> acc;
+  acc.cur = -1;
+  acc.reset();
 
   for (int64_t tile = t0; tile < t1; ++tile) {
     const int64_t base = tile * T;
@@ -356,6 +584,13 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
       misc->nonfinite = 0;
       misc->nqueue = 0;
     }
+    RawTile rt;
+    rt.raw = raw;
+    rt.staged = staged_tile(tile);
+    if (rt.staged) {
+      mbar_wait(mbar, phase);
+      phase ^= 1u;
+    }
     __syncthreads();
 
     // ---------------- A1: group slot of every row + rank within its 32-row unit
@@ -364,9 +599,9 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
       if (li < tn) {
         const int64_t r = base + li;
         bool keep = true;
-        if (p.mask_in) keep = __ldg(p.mask_in + r) != 0ull;  // R21: a row in no world is dropped
+        if (p.mask_in) keep = raw_u64(p, rt, 0, p.mask_in, r, li) != 0ull;  // R21: dropped
         if (keep) {
-          const uint64_t key = row_group_key(p, r);
+          const uint64_t key = raw_group_key(p, rt, r, li);
           const int code = local_code(p, key, lkey, lstate, LH, lprov, Lcap, misc);
           if (code < kOvfBase) {
             s = code - 1;
@@ -457,41 +692,31 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
     __syncthreads();
 
     // ---------------- A2: hash + values, written straight to the slot-sorted position.
-    // pac_hash runs its first draw word inline; rows still needing flips are queued.
+    // pac_hash runs its first draw word inline -- two rows per thread, interleaved for ILP;
+    // rows still needing flips are queued for A3.
     bool big = false, nonfin = false;
-    for (int li = tid; li < T; li += nth) {
-      const unsigned short s = sslot[li];
-      bool pending = false;
-      int pos = 0;
-      if (s != kNone) {
-        const int64_t r = base + li;
-        pos = ucnt[(li >> 5) * Lcap + s] + srank[li];
-        uint64_t m;
-        if (p.mask_in) {
-          m = (uint64_t)__ldg(p.mask_in + r);
-        } else {
-          const HashState h = pac_hash_begin((uint64_t)__ldg(p.pu_key + r), p.salt);
-          m = h.x ^ (((__popcll(h.x) > 32) ? h.x : ~h.x) ^ h.cand);
-          pending = h.k > 0;
-        }
-        smask[pos] = m;
+    auto stage_values = [&](int li, int pos) {
+      const int64_t r = base + li;
 #pragma unroll
-        for (int c = 0; c < NI; ++c) {
-          const long long v = __ldg(p.icol[c] + r);
-          const unsigned long long a = v < 0 ? 0ull - (unsigned long long)v : (unsigned long long)v;
-          maxabs = a > maxabs ? a : maxabs;
-          big |= a >= (1ull << 26);
-          sival[c * TS + pos] = v;
-          si32[c * TS + pos] = (int)v;
-        }
-#pragma unroll
-        for (int c = 0; c < NF; ++c) {
-          const double v = __ldg(p.fcol[c] + r);
-          nonfin |= !finite_bits(v);
-          sfval[c * TS + pos] = v;
-        }
-        if (MM) smval[pos] = __ldg(p.mcol + r);
+      for (int c = 0; c < NI; ++c) {
+        const long long v = (long long)raw_u64(p, rt, 1 + p.n_keys + c, p.icol[c], r, li);
+        const unsigned long long a = v < 0 ? 0ull - (unsigned long long)v : (unsigned long long)v;
+        maxabs = a > maxabs ? a : maxabs;
+        big |= a >= (1ull << 26);
+        sival[c * TS + pos] = v;
+        si32[c * TS + pos] = (int)v;
       }
+#pragma unroll
+      for (int c = 0; c < NF; ++c) {
+        const double v = __longlong_as_double(
+            (long long)raw_u64(p, rt, 1 + p.n_keys + p.ni + c, p.fcol[c], r, li));
+        nonfin |= !finite_bits(v);
+        sfval[c * TS + pos] = v;
+      }
+      if (MM) smval[pos] = __longlong_as_double((long long)raw_u64(p, rt, 1 + p.n_keys + p.ni + p.nf,
+                                                                   p.mcol, r, li));
+    };
+    auto push_queue = [&](bool pending, int pos, int li) {
       const unsigned pm = __ballot_sync(0xffffffffu, pending);
       int qb = 0;
       if (lane == 0 && pm) qb = atomicAdd(&misc->nqueue, __popc(pm));
@@ -500,6 +725,34 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
         qpos[qb] = (unsigned short)pos;
         qrow[qb] = (unsigned short)li;
       }
+    };
+    for (int la = tid; la < T; la += 2 * nth) {
+      const int lb = la + nth;  // T is a multiple of 2 * nth
+      const unsigned short sa = sslot[la], sb = sslot[lb];
+      const int pa = sa != kNone ? ucnt[(la >> 5) * Lcap + sa] + srank[la] : 0;
+      const int pb = sb != kNone ? ucnt[(lb >> 5) * Lcap + sb] + srank[lb] : 0;
+      bool qa = false, qb = false;
+      if (p.mask_in) {
+        if (sa != kNone) smask[pa] = raw_u64(p, rt, 0, p.mask_in, base + la, la);
+        if (sb != kNone) smask[pb] = raw_u64(p, rt, 0, p.mask_in, base + lb, lb);
+      } else {
+        const uint64_t ka = sa != kNone ? raw_u64(p, rt, 0, p.pu_key, base + la, la) : 0ull;
+        const uint64_t kb = sb != kNone ? raw_u64(p, rt, 0, p.pu_key, base + lb, lb) : 0ull;
+        HashState ha, hb;
+        pac_hash_begin2(ka, kb, p.salt, ha, hb);
+        if (sa != kNone) {
+          smask[pa] = ha.x ^ (((__popcll(ha.x) > 32) ? ha.x : ~ha.x) ^ ha.cand);
+          qa = ha.k > 0;
+        }
+        if (sb != kNone) {
+          smask[pb] = hb.x ^ (((__popcll(hb.x) > 32) ? hb.x : ~hb.x) ^ hb.cand);
+          qb = hb.k > 0;
+        }
+      }
+      if (sa != kNone) stage_values(la, pa);
+      if (sb != kNone) stage_values(lb, pb);
+      push_queue(qa, pa, la);
+      push_queue(qb, pb, lb);
     }
     if (NI > 0 && __any_sync(0xffffffffu, big) && lane == 0) misc->big = 1;
     if (NF > 0 && __any_sync(0xffffffffu, nonfin) && lane == 0) misc->nonfinite = 1;
@@ -512,124 +765,41 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
       const int qn = misc->nqueue;
       for (int qi = tid; qi < qn; qi += nth) {
         const int pos = qpos[qi];
-        const uint64_t x = fmix64((uint64_t)__ldg(p.pu_key + base + qrow[qi]) ^ p.salt);
+        const int li = qrow[qi];
+        const uint64_t x = fmix64(raw_u64(p, rt, 0, p.pu_key, base + li, li) ^ p.salt);
         const uint64_t m = smask[pos];
         smask[pos] = pac_hash_finish(x, (__popcll(x) > 32) ? m : ~m, abs(__popcll(m) - 32));
       }
     }
     __syncthreads();
+    // the raw tile buffer is free: stage the next tile while phase C runs
+    if (tid == 0 && staged_tile(tile + 1)) issue_tile(p, raw, mbar, (tile + 1) * T, T);
 
     // ---------------- C: world-parallel runs, transposed "Four Russians" tables
     {
+      RunCtx x;
+      x.smask = smask;
+      x.sival = sival;
+      x.si32 = si32;
+      x.sfval = sfval;
+      x.smval = smval;
+      x.hist = hist;
+      x.offs = offs;
+      x.runoffs = runoffs;
+      x.tcs = tcs;
+      x.TS = TS;
+      x.Lcap = Lcap;
+      x.R = misc->nruns;
       const bool small = (NI == 0) || misc->big == 0;
       const bool fin = (NF == 0) || misc->nonfinite == 0;
-      const int R = misc->nruns;
-      const int r0 = (int)(((long long)R * wid) / nw);
-      const int r1 = (int)(((long long)R * (wid + 1)) / nw);
-      int s = 0;
-      if (r0 < r1) {
-        int lo = 0, hi = Lcap;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (runoffs[mid] <= r0) lo = mid; else hi = mid - 1;
-        }
-        s = lo;
-      }
-      const double db0 = ib0, db1 = ib1, db2 = ib2, db3 = ib3;
-      for (int r = r0; r < r1; ++r) {
-        while (runoffs[s + 1] <= r) ++s;
-        if (s != cur) {
-          flush();
-          cur = s;
-        }
-        const int k0 = 32 * (r - runoffs[s]);
-        const int beg = offs[s] + k0;
-        const int len = min(32, hist[s] - k0);
-        const uint64_t m = lane < len ? smask[beg + lane] : 0ull;
-        uint32_t P = (uint32_t)m, Q = (uint32_t)(m >> 32);
-        transpose2x32(P, Q, tcs, lane);
-        c0 += __popc(P);
-        c1 += __popc(Q);
-        // nibble indices: table A (lanes 0-15) covers rows 8q..8q+3, B (16-31) rows 8q+4..8q+7;
-        // shfl uses only the low 5 bits of the source lane.
-        const uint32_t PA = P & 0x0F0F0F0Fu, PB = ((P >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
-        const uint32_t QA = Q & 0x0F0F0F0Fu, QB = ((Q >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
-        const int nq = (len + 7) >> 3;
-        int rs0[NI > 0 ? NI : 1], rs1[NI > 0 ? NI : 1];
-#pragma unroll
-        for (int c = 0; c < NI; ++c) rs0[c] = rs1[c] = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (q >= nq) break;
-          const int a0 = (int)(PA >> (8 * q)), b0 = (int)(PB >> (8 * q));
-          const int a1 = (int)(QA >> (8 * q)), b1 = (int)(QB >> (8 * q));
-          const int row = beg + 8 * q + tsrc;
-#pragma unroll
-          for (int c = 0; c < NI; ++c) {
-            if (small) {
-              const int4 v = *(const int4*)(si32 + c * TS + row);
-              const int t = v.x * ib0 + v.y * ib1 + v.z * ib2 + v.w * ib3;
-              rs0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
-              rs1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
-            } else {
-              const longlong2 u = *(const longlong2*)(sival + c * TS + row);
-              const longlong2 w = *(const longlong2*)(sival + c * TS + row + 2);
-              const long long t = u.x * ib0 + u.y * ib1 + w.x * ib2 + w.y * ib3;
-              ia0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
-              ia1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < NF; ++c) {
-            const double2 u = *(const double2*)(sfval + c * TS + row);
-            const double2 w = *(const double2*)(sfval + c * TS + row + 2);
-            double t;
-            if (fin) {  // exact: 0*v + t == t and 1*v + t == v + t for finite v
-              t = fma(db3, w.y, fma(db2, w.x, fma(db1, u.y, db0 * u.x)));
-            } else {
-              t = ib0 ? u.x : 0.0;
-              if (ib1) t += u.y;
-              if (ib2) t += w.x;
-              if (ib3) t += w.y;
-            }
-            fa0[c] += shfl_d(t, a0);
-            fa0[c] += shfl_d(t, b0);
-            fa1[c] += shfl_d(t, a1);
-            fa1[c] += shfl_d(t, b1);
-          }
-          if (MM) {
-            const double2 u = *(const double2*)(smval + row);
-            const double2 w = *(const double2*)(smval + row + 2);
-            if (MM & 1) {
-              double t = ib0 ? u.x : INFINITY;
-              if (ib1) t = fmin(t, u.y);
-              if (ib2) t = fmin(t, w.x);
-              if (ib3) t = fmin(t, w.y);
-              mn0 = fmin(mn0, fmin(shfl_d(t, a0), shfl_d(t, b0)));
-              mn1 = fmin(mn1, fmin(shfl_d(t, a1), shfl_d(t, b1)));
-            }
-            if (MM & 2) {
-              double t = ib0 ? u.x : -INFINITY;
-              if (ib1) t = fmax(t, u.y);
-              if (ib2) t = fmax(t, w.x);
-              if (ib3) t = fmax(t, w.y);
-              mx0 = fmax(mx0, fmax(shfl_d(t, a0), shfl_d(t, b0)));
-              mx1 = fmax(mx1, fmax(shfl_d(t, a1), shfl_d(t, b1)));
-            }
-          }
-        }
-        if (small) {
-#pragma unroll
-          for (int c = 0; c < NI; ++c) {
-            ia0[c] += rs0[c];
-            ia1[c] += rs1[c];
-          }
-        }
-      }
+      if (small && fin) run_tiles<NI, NF, MM, true, true>(acc, x, cnt, isum, fsum, emin, emax, wid, nw, lane);
+      else if (small) run_tiles<NI, NF, MM, true, false>(acc, x, cnt, isum, fsum, emin, emax, wid, nw, lane);
+      else if (fin) run_tiles<NI, NF, MM, false, true>(acc, x, cnt, isum, fsum, emin, emax, wid, nw, lane);
+      else run_tiles<NI, NF, MM, false, false>(acc, x, cnt, isum, fsum, emin, emax, wid, nw, lane);
     }
     __syncthreads();
   }
-  flush();
+  acc.flush(cnt, isum, fsum, emin, emax, Lcap, lane);
   __syncthreads();
 
   // ---------------- CTA table -> provisional HBM table
@@ -1090,7 +1260,12 @@ static WsLayout ws_layout(const AccSet& A, int64_t G_cap) {
   return w;
 }
 
-static SmemLayout make_layout(const AccSet& A, int T, int Lcap) {
+static int raw_tile_bytes(const AccSet& A, int T, int key_bytes) {
+  const int cols8 = 1 + A.ni + A.nf + ((A.has_min || A.has_max) ? 1 : 0);
+  return cols8 * T * 8 + ((key_bytes * T + 15) & ~15) + 16 * PAC_MAX_KEYS;
+}
+
+static SmemLayout make_layout(const AccSet& A, int T, int Lcap, int key_bytes = 8) {
   SmemLayout L{};
   L.T = T;
   L.TS = T + 8 * Lcap;  // slot-sorted staging, each slot padded to a multiple of 8 rows
@@ -1126,29 +1301,36 @@ static SmemLayout make_layout(const AccSet& A, int T, int Lcap) {
   L.o_slot = take(T * 2);
   L.o_rank = take(T);
   L.o_tcs = take(5 * 32 * 8);
+  L.o_raw = take(raw_tile_bytes(A, T, key_bytes));
+  L.o_mbar = take(16);
   L.o_misc = take(sizeof(Misc));
   L.bytes = off;
   return L;
 }
 
-// Local slot capacity: min(G_cap, 256).  Prefer a layout that leaves room for three CTAs
-// per SM; otherwise one or two CTAs with as many slots as fit (tile 1024, else 512).
-static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, SmemLayout* out) {
+// Local slot capacity: min(G_cap, 256).  Preference: all wanted slots with three CTAs per SM
+// (tile 1024, then 512), then two CTAs per SM, then one CTA per SM with as many slots as
+// fit.  PAC_TILE=512|1024 forces the tile size (experiments).
+static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, int key_bytes, SmemLayout* out) {
   const int want = (int)std::min<int64_t>(std::max<int64_t>(G_cap, 1), 256);
-  const int third = smem_max / 3 - 2048;
-  for (int T : {1024, 512}) {
-    SmemLayout L = make_layout(A, T, want);
-    if (L.bytes <= third) {
-      *out = L;
-      return true;
+  const char* force = getenv("PAC_TILE");
+  const int tiles_fixed[2] = {force ? atoi(force) : 1024, force ? atoi(force) : 512};
+  for (int per_sm : {3, 2}) {
+    const int budget = smem_max / per_sm - 2048;
+    for (int T : tiles_fixed) {
+      SmemLayout L = make_layout(A, T, want, key_bytes);
+      if (L.bytes <= budget) {
+        *out = L;
+        return true;
+      }
     }
   }
   int best = 0, bestT = 0;
-  for (int T : {1024, 512}) {
+  for (int T : tiles_fixed) {
     int lo = 0, hi = want;
     while (lo < hi) {
       int mid = (lo + hi + 1) / 2;
-      if (make_layout(A, T, mid).bytes <= smem_max) lo = mid; else hi = mid - 1;
+      if (make_layout(A, T, mid, key_bytes).bytes <= smem_max) lo = mid; else hi = mid - 1;
     }
     if (lo > best) {
       best = lo;
@@ -1156,7 +1338,7 @@ static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, SmemLayo
     }
   }
   if (best < 1) return false;
-  *out = make_layout(A, bestT, best);
+  *out = make_layout(A, bestT, best, key_bytes);
   return true;
 }
 
@@ -1351,7 +1533,30 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
       profile_end(st);
     } else {
       SmemLayout L{};
-      if (!choose_layout(A, G_cap, smem_max, &L)) return PAC_E_INVAL;
+      if (!choose_layout(A, G_cap, smem_max, width, &L)) return PAC_E_INVAL;
+      // raw columns staged per tile by TMA (k_agg_tiles reads them from smem)
+      {
+        int off = 0;
+        bool aligned = true;
+        auto add = [&](const void* col, int eb) {
+          p.raw_src[p.nraw] = col;
+          p.raw_eb[p.nraw] = eb;
+          p.raw_off[p.nraw] = off;
+          off += (L.T * eb + 15) & ~15;
+          aligned = aligned && (((uintptr_t)col) & 15) == 0;
+          ++p.nraw;
+        };
+        p.nraw = 0;
+        add(d_mask ? (const void*)d_mask : (const void*)d_pu_key, 8);
+        for (int c = 0; c < n_keys; ++c) add(keys[c].d_col, keys[c].elem_bytes);
+        for (int c = 0; c < A.ni; ++c) add(A.icol[c], 8);
+        for (int c = 0; c < A.nf; ++c) add(A.fcol[c], 8);
+        if (A.has_min || A.has_max) add(A.mcol, 8);
+        int copied = 0;
+        for (int i = 0; i < p.nraw; ++i) copied += L.T * p.raw_eb[i];
+        p.raw_bytes = copied;
+        p.tma_ok = (aligned && !getenv("PAC_NO_TMA")) ? 1 : 0;
+      }
       if (getenv("PAC_DEBUG"))
         fprintf(stderr, "[libpac] k_agg_tiles<%d,%d,%d> T=%d Lcap=%d LH=%d smem=%d B (G_cap=%lld)\n", A.ni,
                 A.nf, (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0), L.T, L.Lcap, L.LH, L.bytes, (long long)G_cap);

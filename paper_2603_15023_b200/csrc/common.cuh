@@ -78,6 +78,32 @@ __device__ __forceinline__ uint64_t pac_hash_finish(uint64_t x, uint64_t cand, i
   return x ^ (cand0 ^ cand);
 }
 
+// Two independent keys, their draws interleaved so the two dependency chains overlap.
+__device__ __forceinline__ void draw_step(uint64_t w, int t, uint64_t& cand, int& k) {
+  const uint32_t p = (uint32_t)(w >> (6 * t)) & 63u;
+  uint64_t hit = cand & (1ull << p);
+  hit = (k > 0) ? hit : 0ull;
+  cand ^= hit;
+  k -= (hit != 0ull) ? 1 : 0;
+}
+
+__device__ __forceinline__ void pac_hash_begin2(uint64_t ka, uint64_t kb, uint64_t salt, HashState& a,
+                                                HashState& b) {
+  a.x = fmix64(ka ^ salt);
+  b.x = fmix64(kb ^ salt);
+  const int ca = __popcll(a.x), cb = __popcll(b.x);
+  a.k = (ca > 32) ? (ca - 32) : (32 - ca);
+  b.k = (cb > 32) ? (cb - 32) : (32 - cb);
+  a.cand = (ca > 32) ? a.x : ~a.x;
+  b.cand = (cb > 32) ? b.x : ~b.x;
+  const uint64_t wa = fmix64(a.x ^ kDrawSeed), wb = fmix64(b.x ^ kDrawSeed);
+#pragma unroll
+  for (int t = 0; t < 10; ++t) {
+    draw_step(wa, t, a.cand, a.k);
+    draw_step(wb, t, b.cand, b.k);
+  }
+}
+
 __device__ __forceinline__ uint64_t pac_hash_dev(uint64_t key, uint64_t salt) {
   HashState h = pac_hash_begin(key, salt);
   const uint64_t cand0 = (__popcll(h.x) > 32) ? h.x : ~h.x;
