@@ -49,6 +49,7 @@ struct AggPlan {
   // raw input columns staged per tile by 1-D TMA bulk copies (k_agg_tiles):
   // 0 = pu_key or mask, 1..n_keys = key columns, then int64 sums, f64 sums, min/max column
   int nraw, tma_ok;
+  int ablate;  // profiling only (PAC_ABLATE): 1 = no draws, 2 = no A3, 4 = no phase C
   const void* raw_src[1 + PAC_MAX_KEYS + 5];
   int raw_eb[1 + PAC_MAX_KEYS + 5];
   int raw_off[1 + PAC_MAX_KEYS + 5];  // byte offset of the column inside the raw tile buffer
@@ -237,39 +238,6 @@ __device__ __forceinline__ void issue_tile(const AggPlan& p, unsigned char* raw,
   mbar_expect_tx(mbar, (uint32_t)p.raw_bytes);
   for (int i = 0; i < p.nraw; ++i)
     bulk_g2s(raw + p.raw_off[i], (const char*)p.raw_src[i] + base * p.raw_eb[i], (uint32_t)(T * p.raw_eb[i]), mbar);
-}
-
-// Row accessors: staged tiles read the raw smem copy, other tiles read global memory.
-struct RawTile {
-  const unsigned char* raw;
-  bool staged;
-};
-__device__ __forceinline__ uint64_t raw_u64(const AggPlan& p, const RawTile& t, int col, const void* g,
-                                            int64_t r, int li) {
-  return t.staged ? ((const unsigned long long*)(t.raw + p.raw_off[col]))[li]
-                  : (uint64_t)__ldg((const unsigned long long*)g + r);
-}
-__device__ __forceinline__ uint64_t raw_group_key(const AggPlan& p, const RawTile& t, int64_t r, int li) {
-  uint64_t packed = 0;
-#pragma unroll
-  for (int c = 0; c < PAC_MAX_KEYS; ++c) {
-    if (c < p.n_keys) {
-      const int w = p.key_bytes[c];
-      uint64_t v;
-      if (t.staged) {
-        const unsigned char* col = t.raw + p.raw_off[1 + c];
-        if (w == 1) v = col[li];
-        else if (w == 2) v = ((const unsigned short*)col)[li];
-        else if (w == 4) v = ((const unsigned*)col)[li];
-        else v = ((const unsigned long long*)col)[li];
-        v ^= 1ull << (8 * w - 1);
-      } else {
-        v = load_key_part(p.key_col[c], w, r);
-      }
-      packed = (w == 8) ? v : ((packed << (8 * w)) | v);
-    }
-  }
-  return packed;
 }
 
 // ------------------------------------------------------------------ k_agg_tiles (v3)
@@ -499,59 +467,318 @@ __device__ __forceinline__ void run_tiles(WarpAcc<NI, NF, MM>& acc, const RunCtx
   }
 }
 
-template <int NI, int NF, int MM>
-__global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLayout L) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* lkey = (unsigned long long*)(smem + L.o_lkey);
-  int* lstate = (int*)(smem + L.o_lstate);
-  int* lprov = (int*)(smem + L.o_lprov);
-  unsigned long long* lrows = (unsigned long long*)(smem + L.o_lrows);
-  unsigned* cnt = (unsigned*)(smem + L.o_cnt);
-  unsigned long long* isum = (unsigned long long*)(smem + L.o_isum);
-  double* fsum = (double*)(smem + L.o_fsum);
-  long long* emin = (long long*)(smem + L.o_min);
-  long long* emax = (long long*)(smem + L.o_max);
-  unsigned long long* smask = (unsigned long long*)(smem + L.o_mask);  // [TS] slot-sorted
-  long long* sival = (long long*)(smem + L.o_ival);                     // [NI][TS]
-  int* si32 = (int*)(smem + L.o_i32);                                   // [NI][TS]
-  double* sfval = (double*)(smem + L.o_fval);                           // [NF][TS]
-  double* smval = (double*)(smem + L.o_mval);                           // [TS]
-  unsigned short* sslot = (unsigned short*)(smem + L.o_slot);           // [T]
-  unsigned char* srank = (unsigned char*)(smem + L.o_rank);             // [T]
-  unsigned short* ucnt = (unsigned short*)(smem + L.o_ucnt);            // [units][Lcap]
-  unsigned short* qpos = (unsigned short*)(smem + L.o_queue);           // [T]
-  unsigned short* qrow = qpos + L.T;                                    // [T]
-  int* hist = (int*)(smem + L.o_hist);
-  int* offs = (int*)(smem + L.o_offs);
-  int* runoffs = (int*)(smem + L.o_runoffs);
-  Misc* misc = (Misc*)(smem + L.o_misc);
-  unsigned char* raw = smem + L.o_raw;
-  unsigned long long* mbar = (unsigned long long*)(smem + L.o_mbar);
+struct TileSmem {
+  unsigned long long* lkey;
+  int* lstate;
+  int* lprov;
+  unsigned long long* lrows;
+  unsigned* cnt;
+  unsigned long long* isum;
+  double* fsum;
+  long long* emin;
+  long long* emax;
+  unsigned long long* smask;  // [TS] slot-sorted masks
+  long long* sival;           // [NI][TS]
+  int* si32;                  // [NI][TS]
+  double* sfval;              // [NF][TS]
+  double* smval;              // [TS]
+  unsigned short* sslot;      // [T]
+  unsigned char* srank;       // [T]
+  unsigned short* ucnt;       // [units][Lcap]
+  unsigned short* qpos;       // [T]
+  unsigned short* qrow;       // [T]
+  int* hist;
+  int* offs;
+  int* runoffs;
+  uint2* tcs;
+  Misc* misc;
+  const unsigned char* raw;   // staged raw tile: 8-byte columns k at k*T*8, then key columns
+};
 
+// Column k of the tile: 0 = pu_key/mask, 1..NI int64 sums, NI+1..NI+NF f64 sums, then the
+// MIN/MAX column; group-key columns after them.  Staged tiles read the TMA copy in smem.
+template <bool STAGED>
+struct TileCols {
+  const AggPlan* p;
+  const unsigned char* raw;
+  int64_t base;
+  int T;
+  __device__ __forceinline__ uint64_t w8(int k, int li) const {
+    if (STAGED) return ((const unsigned long long*)raw)[(size_t)k * T + li];
+    return (uint64_t)__ldg((const unsigned long long*)p->raw_src[k] + base + li);
+  }
+  __device__ __forceinline__ uint64_t group_key(int k0, int li) const {
+    uint64_t packed = 0;
+#pragma unroll
+    for (int c = 0; c < PAC_MAX_KEYS; ++c) {
+      if (c < p->n_keys) {
+        const int w = p->key_bytes[c];
+        uint64_t v;
+        if (STAGED) {
+          const unsigned char* col = raw + p->raw_off[k0 + c];
+          if (w == 1) v = col[li];
+          else if (w == 2) v = ((const unsigned short*)col)[li];
+          else if (w == 4) v = ((const unsigned*)col)[li];
+          else v = ((const unsigned long long*)col)[li];
+          v ^= 1ull << (8 * w - 1);
+        } else {
+          v = load_key_part(p->key_col[c], w, base + li);
+        }
+        packed = (w == 8) ? v : ((packed << (8 * w)) | v);
+      }
+    }
+    return packed;
+  }
+};
+
+// A1 (slots + ranks), B (offsets), A2 (hash word 0 + sorted staging), A3 (stragglers) of one
+// tile.  Leaves the slot-sorted tile in smem and the run table for phase C.
+template <int NI, int NF, int MM, bool STAGED>
+__device__ __forceinline__ void tile_front(const AggPlan& p, const TileSmem& sm, const SmemLayout& L, int64_t base,
+                                           int tn, unsigned long long& maxabs) {
   const int tid = threadIdx.x, nth = blockDim.x;
-  const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  const int lane = tid & 31, wid = tid >> 5;
   const int T = L.T, TS = L.TS, Lcap = L.Lcap, LH = L.LH;
   const int units = T >> 5;
   const unsigned short kNone = 0xFFFF;
   const unsigned lt_mask = (1u << lane) - 1u;
+  constexpr int KF = 1 + NI;             // first f64 sum column
+  constexpr int KM = 1 + NI + NF;        // min/max column
+  constexpr int KK = 1 + NI + NF + (MM ? 1 : 0);  // first group-key column
+  TileCols<STAGED> tc{&p, sm.raw, base, T};
+  Misc* misc = sm.misc;
 
-  for (int i = tid; i < LH; i += nth) lstate[i] = 0;
-  for (int i = tid; i < Lcap; i += nth) lrows[i] = 0;
+  // ---------------- A1: group slot of every row + rank within its 32-row unit
+  for (int li = tid; li < T; li += nth) {
+    int s = -1;
+    if (li < tn) {
+      bool keep = true;
+      if (p.mask_in) keep = tc.w8(0, li) != 0ull;  // R21: a row in no world is dropped
+      if (keep) {
+        const uint64_t key = tc.group_key(KK, li);
+        const int code = local_code(p, key, sm.lkey, sm.lstate, LH, sm.lprov, Lcap, misc);
+        if (code < kOvfBase) {
+          s = code - 1;
+        } else {  // no local slot: straight to the HBM table (rare)
+          long long iv[NI > 0 ? NI : 1];
+          double fv[NF > 0 ? NF : 1];
+#pragma unroll
+          for (int c = 0; c < NI; ++c) iv[c] = (long long)tc.w8(1 + c, li);
+#pragma unroll
+          for (int c = 0; c < NF; ++c) fv[c] = __longlong_as_double((long long)tc.w8(KF + c, li));
+          const double mv = MM ? __longlong_as_double((long long)tc.w8(KM, li)) : 0.0;
+          const uint64_t m = p.mask_in ? tc.w8(0, li) : pac_hash_dev(tc.w8(0, li), p.salt);
+          global_row_update<NI, NF, MM>(p, code - kOvfBase - 1, m, iv, fv, mv);
+        }
+      }
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, s >= 0 ? (unsigned)s : 0x10000u + lane);
+    if (s >= 0) {
+      sm.srank[li] = (unsigned char)__popc(peers & lt_mask);
+      if ((peers & lt_mask) == 0) sm.ucnt[(li >> 5) * Lcap + s] = (unsigned short)__popc(peers);
+    }
+    sm.sslot[li] = s >= 0 ? (unsigned short)s : kNone;
+  }
+  __syncthreads();
+
+  // ---------------- B: slot totals, 8-row padded offsets, run offsets, unit positions
+  for (int s = tid; s < Lcap; s += nth) {
+    int tot = 0;
+    for (int u = 0; u < units; ++u) tot += sm.ucnt[u * Lcap + s];
+    sm.hist[s] = tot;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int per = (Lcap + 31) / 32;
+    const int s0 = lane * per;
+    int hsum = 0, rsum = 0;
+    for (int s = s0; s < min(Lcap, s0 + per); ++s) {
+      hsum += (sm.hist[s] + 7) & ~7;
+      rsum += (sm.hist[s] + 31) >> 5;
+    }
+    int hx = hsum, rx = rsum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, hx, d);
+      const int b = __shfl_up_sync(0xffffffffu, rx, d);
+      if (lane >= d) {
+        hx += a;
+        rx += b;
+      }
+    }
+    hx -= hsum;
+    rx -= rsum;
+    for (int s = s0; s < min(Lcap, s0 + per); ++s) {
+      sm.offs[s] = hx;
+      sm.runoffs[s] = rx;
+      sm.lrows[s] += (unsigned long long)sm.hist[s];
+      hx += (sm.hist[s] + 7) & ~7;
+      rx += (sm.hist[s] + 31) >> 5;
+    }
+    if (lane == 31) {
+      sm.runoffs[Lcap] = rx;
+      misc->nruns = rx;
+    }
+  }
+  __syncthreads();
+  for (int s = tid; s < Lcap; s += nth) {
+    const int o0 = sm.offs[s];
+    int o = o0;
+    for (int u = 0; u < units; ++u) {
+      const int c = sm.ucnt[u * Lcap + s];
+      sm.ucnt[u * Lcap + s] = (unsigned short)o;
+      o += c;
+    }
+    for (int q = o; q < o0 + ((sm.hist[s] + 7) & ~7); ++q) {  // zero padding rows (mask 0)
+      sm.smask[q] = 0;
+#pragma unroll
+      for (int c = 0; c < NI; ++c) {
+        sm.sival[c * TS + q] = 0;
+        sm.si32[c * TS + q] = 0;
+      }
+#pragma unroll
+      for (int c = 0; c < NF; ++c) sm.sfval[c * TS + q] = 0.0;
+      if (MM) sm.smval[q] = 0.0;
+    }
+  }
+  __syncthreads();
+
+  // ---------------- A2: hash word 0 (two rows per thread, interleaved) + values, written
+  // straight to the slot-sorted position; rows still needing flips are queued for A3.
+  bool big = false, nonfin = false;
+  for (int la = tid; la < T; la += 2 * nth) {
+    const int lb = la + nth;  // T is a multiple of 2 * nth
+    const unsigned short sa = sm.sslot[la], sb = sm.sslot[lb];
+    const int pa = sa != kNone ? sm.ucnt[(la >> 5) * Lcap + sa] + sm.srank[la] : 0;
+    const int pb = sb != kNone ? sm.ucnt[(lb >> 5) * Lcap + sb] + sm.srank[lb] : 0;
+    bool qa = false, qb = false;
+    const uint64_t ka = sa != kNone ? tc.w8(0, la) : 0ull;
+    const uint64_t kb = sb != kNone ? tc.w8(0, lb) : 0ull;
+    uint64_t ma = ka, mb = kb;
+    if (!p.mask_in) {
+      HashState ha, hb;
+      if (p.ablate & 1) {
+        ha.x = ka; ha.cand = ka; ha.k = 0; hb.x = kb; hb.cand = kb; hb.k = 0;
+      } else {
+        pac_hash_begin2(ka, kb, p.salt, ha, hb);
+      }
+      ma = ha.x ^ (((__popcll(ha.x) > 32) ? ha.x : ~ha.x) ^ ha.cand);
+      mb = hb.x ^ (((__popcll(hb.x) > 32) ? hb.x : ~hb.x) ^ hb.cand);
+      qa = sa != kNone && ha.k > 0;
+      qb = sb != kNone && hb.k > 0;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int li = h ? lb : la;
+      const int pos = h ? pb : pa;
+      if ((h ? sb : sa) == kNone) continue;
+      sm.smask[pos] = h ? mb : ma;
+#pragma unroll
+      for (int c = 0; c < NI; ++c) {
+        const long long v = (long long)tc.w8(1 + c, li);
+        const unsigned long long a = v < 0 ? 0ull - (unsigned long long)v : (unsigned long long)v;
+        maxabs = a > maxabs ? a : maxabs;
+        big |= a >= (1ull << 26);
+        sm.sival[c * TS + pos] = v;
+        sm.si32[c * TS + pos] = (int)v;
+      }
+#pragma unroll
+      for (int c = 0; c < NF; ++c) {
+        const double v = __longlong_as_double((long long)tc.w8(KF + c, li));
+        nonfin |= !finite_bits(v);
+        sm.sfval[c * TS + pos] = v;
+      }
+      if (MM) sm.smval[pos] = __longlong_as_double((long long)tc.w8(KM, li));
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool pend = h ? qb : qa;
+      const unsigned pm = __ballot_sync(0xffffffffu, pend);
+      int qbase = 0;
+      if (lane == 0 && pm) qbase = atomicAdd(&misc->nqueue, __popc(pm));
+      qbase = __shfl_sync(0xffffffffu, qbase, 0) + __popc(pm & lt_mask);
+      if (pend) {
+        sm.qpos[qbase] = (unsigned short)(h ? pb : pa);
+        sm.qrow[qbase] = (unsigned short)(h ? lb : la);
+      }
+    }
+  }
+  if (NI > 0 && __any_sync(0xffffffffu, big) && lane == 0) misc->big = 1;
+  if (NF > 0 && __any_sync(0xffffffffu, nonfin) && lane == 0) misc->nonfinite = 1;
+  __syncthreads();
+
+  // ---------------- A3: finish the queued masks.  State re-derived from the key and the
+  // partial mask: cand = majority positions of the current word, k = |popcount - 32|.
+  if (!(p.ablate & 2)) {
+    const int qn = misc->nqueue;
+    for (int qi = tid; qi < qn; qi += nth) {
+      const int pos = sm.qpos[qi];
+      const uint64_t x = fmix64(tc.w8(0, sm.qrow[qi]) ^ p.salt);
+      const uint64_t m = sm.smask[pos];
+      sm.smask[pos] = pac_hash_finish(x, (__popcll(x) > 32) ? m : ~m, abs(__popcll(m) - 32));
+    }
+  }
+  __syncthreads();
+}
+
+template <int NI, int NF, int MM>
+__global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLayout L) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  TileSmem sm;
+  sm.lkey = (unsigned long long*)(smem + L.o_lkey);
+  sm.lstate = (int*)(smem + L.o_lstate);
+  sm.lprov = (int*)(smem + L.o_lprov);
+  sm.lrows = (unsigned long long*)(smem + L.o_lrows);
+  sm.cnt = (unsigned*)(smem + L.o_cnt);
+  sm.isum = (unsigned long long*)(smem + L.o_isum);
+  sm.fsum = (double*)(smem + L.o_fsum);
+  sm.emin = (long long*)(smem + L.o_min);
+  sm.emax = (long long*)(smem + L.o_max);
+  sm.smask = (unsigned long long*)(smem + L.o_mask);
+  sm.sival = (long long*)(smem + L.o_ival);
+  sm.si32 = (int*)(smem + L.o_i32);
+  sm.sfval = (double*)(smem + L.o_fval);
+  sm.smval = (double*)(smem + L.o_mval);
+  sm.sslot = (unsigned short*)(smem + L.o_slot);
+  sm.srank = (unsigned char*)(smem + L.o_rank);
+  sm.ucnt = (unsigned short*)(smem + L.o_ucnt);
+  sm.qpos = (unsigned short*)(smem + L.o_queue);
+  sm.qrow = sm.qpos + L.T;
+  sm.hist = (int*)(smem + L.o_hist);
+  sm.offs = (int*)(smem + L.o_offs);
+  sm.runoffs = (int*)(smem + L.o_runoffs);
+  sm.tcs = (uint2*)(smem + L.o_tcs);
+  sm.misc = (Misc*)(smem + L.o_misc);
+  unsigned char* raw = smem + L.o_raw;
+  sm.raw = raw;
+  unsigned long long* mbar = (unsigned long long*)(smem + L.o_mbar);
+  Misc* misc = sm.misc;
+
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  const int T = L.T, Lcap = L.Lcap, LH = L.LH;
+  const int units = T >> 5;
+
+  for (int i = tid; i < LH; i += nth) sm.lstate[i] = 0;
+  for (int i = tid; i < Lcap; i += nth) sm.lrows[i] = 0;
   for (int i = tid; i < Lcap * kM; i += nth) {
-    cnt[i] = 0;
+    sm.cnt[i] = 0;
 #pragma unroll
-    for (int c = 0; c < NI; ++c) isum[(size_t)c * Lcap * kM + i] = 0;
+    for (int c = 0; c < NI; ++c) sm.isum[(size_t)c * Lcap * kM + i] = 0;
 #pragma unroll
-    for (int c = 0; c < NF; ++c) fsum[(size_t)c * Lcap * kM + i] = 0.0;
-    if (MM & 1) emin[i] = kEncPosInf;
-    if (MM & 2) emax[i] = kEncNegInf;
+    for (int c = 0; c < NF; ++c) sm.fsum[(size_t)c * Lcap * kM + i] = 0.0;
+    if (MM & 1) sm.emin[i] = kEncPosInf;
+    if (MM & 2) sm.emax[i] = kEncNegInf;
+  }
+  if (tid < 32) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) sm.tcs[i * 32 + tid] = transpose_const(tid, i);
   }
   if (tid == 0) {
     misc->nlocal = 0;
     misc->ndict = 0;
   }
   unsigned long long maxabs = 0;
-  __syncthreads();
 
   const int64_t ntiles = (p.n_rows + T - 1) / T;
   const int64_t t_per = (ntiles + gridDim.x - 1) / gridDim.x;
@@ -564,13 +791,8 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
     mbar_init(mbar, 1);
     if (staged_tile(t0)) issue_tile(p, raw, mbar, t0 * T, T);
   }
+  __syncthreads();
 
-  // run-processing state of this warp (lane: worlds lane and lane+32)
-  uint2* tcs = (uint2*)(smem + L.o_tcs);
-  if (tid < 32) {
-#pragma unroll
-    for (int i = 0; i < 5; ++i) tcs[i * 32 + tid] = transpose_const(tid, i);
-  }
   WarpAcc<NI, NF, MM> acc;
   acc.cur = -1;
   acc.reset();
@@ -578,228 +800,52 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
   for (int64_t tile = t0; tile < t1; ++tile) {
     const int64_t base = tile * T;
     const int tn = (int)min((int64_t)T, p.n_rows - base);
-    for (int i = tid; i < units * Lcap; i += nth) ucnt[i] = 0;
+    for (int i = tid; i < units * Lcap; i += nth) sm.ucnt[i] = 0;
     if (tid == 0) {
       misc->big = 0;
       misc->nonfinite = 0;
       misc->nqueue = 0;
     }
-    RawTile rt;
-    rt.raw = raw;
-    rt.staged = staged_tile(tile);
-    if (rt.staged) {
+    const bool staged = staged_tile(tile);
+    if (staged) {
       mbar_wait(mbar, phase);
       phase ^= 1u;
     }
     __syncthreads();
-
-    // ---------------- A1: group slot of every row + rank within its 32-row unit
-    for (int li = tid; li < T; li += nth) {
-      int s = -1;
-      if (li < tn) {
-        const int64_t r = base + li;
-        bool keep = true;
-        if (p.mask_in) keep = raw_u64(p, rt, 0, p.mask_in, r, li) != 0ull;  // R21: dropped
-        if (keep) {
-          const uint64_t key = raw_group_key(p, rt, r, li);
-          const int code = local_code(p, key, lkey, lstate, LH, lprov, Lcap, misc);
-          if (code < kOvfBase) {
-            s = code - 1;
-          } else {  // no local slot: straight to the HBM table (rare)
-            long long iv[NI > 0 ? NI : 1];
-            double fv[NF > 0 ? NF : 1];
-#pragma unroll
-            for (int c = 0; c < NI; ++c) iv[c] = __ldg(p.icol[c] + r);
-#pragma unroll
-            for (int c = 0; c < NF; ++c) fv[c] = __ldg(p.fcol[c] + r);
-            const double mv = MM ? __ldg(p.mcol + r) : 0.0;
-            const uint64_t m = p.mask_in ? (uint64_t)__ldg(p.mask_in + r)
-                                         : pac_hash_dev((uint64_t)__ldg(p.pu_key + r), p.salt);
-            global_row_update<NI, NF, MM>(p, code - kOvfBase - 1, m, iv, fv, mv);
-          }
-        }
-      }
-      const unsigned peers = __match_any_sync(0xffffffffu, s >= 0 ? (unsigned)s : 0x10000u + lane);
-      if (s >= 0) {
-        srank[li] = (unsigned char)__popc(peers & lt_mask);
-        if ((peers & lt_mask) == 0) ucnt[(li >> 5) * Lcap + s] = (unsigned short)__popc(peers);
-      }
-      sslot[li] = s >= 0 ? (unsigned short)s : kNone;
-    }
-    __syncthreads();
-
-    // ---------------- B: slot totals, 8-row padded offsets, run offsets, unit positions
-    for (int s = tid; s < Lcap; s += nth) {
-      int tot = 0;
-      for (int u = 0; u < units; ++u) tot += ucnt[u * Lcap + s];
-      hist[s] = tot;
-    }
-    __syncthreads();
-    if (wid == 0) {
-      const int per = (Lcap + 31) / 32;
-      const int s0 = lane * per;
-      int hsum = 0, rsum = 0;
-      for (int s = s0; s < min(Lcap, s0 + per); ++s) {
-        hsum += (hist[s] + 7) & ~7;
-        rsum += (hist[s] + 31) >> 5;
-      }
-      int hx = hsum, rx = rsum;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int a = __shfl_up_sync(0xffffffffu, hx, d);
-        const int b = __shfl_up_sync(0xffffffffu, rx, d);
-        if (lane >= d) {
-          hx += a;
-          rx += b;
-        }
-      }
-      hx -= hsum;
-      rx -= rsum;
-      for (int s = s0; s < min(Lcap, s0 + per); ++s) {
-        offs[s] = hx;
-        runoffs[s] = rx;
-        lrows[s] += (unsigned long long)hist[s];
-        hx += (hist[s] + 7) & ~7;
-        rx += (hist[s] + 31) >> 5;
-      }
-      if (lane == 31) {
-        runoffs[Lcap] = rx;
-        misc->nruns = rx;
-      }
-    }
-    __syncthreads();
-    for (int s = tid; s < Lcap; s += nth) {
-      const int o0 = offs[s];
-      int o = o0;
-      for (int u = 0; u < units; ++u) {
-        const int c = ucnt[u * Lcap + s];
-        ucnt[u * Lcap + s] = (unsigned short)o;
-        o += c;
-      }
-      // zero the padding rows up to the next multiple of 8 (mask 0 = in no world)
-      for (int q = o; q < o0 + ((hist[s] + 7) & ~7); ++q) {
-        smask[q] = 0;
-#pragma unroll
-        for (int c = 0; c < NI; ++c) {
-          sival[c * TS + q] = 0;
-          si32[c * TS + q] = 0;
-        }
-#pragma unroll
-        for (int c = 0; c < NF; ++c) sfval[c * TS + q] = 0.0;
-        if (MM) smval[q] = 0.0;
-      }
-    }
-    __syncthreads();
-
-    // ---------------- A2: hash + values, written straight to the slot-sorted position.
-    // pac_hash runs its first draw word inline -- two rows per thread, interleaved for ILP;
-    // rows still needing flips are queued for A3.
-    bool big = false, nonfin = false;
-    auto stage_values = [&](int li, int pos) {
-      const int64_t r = base + li;
-#pragma unroll
-      for (int c = 0; c < NI; ++c) {
-        const long long v = (long long)raw_u64(p, rt, 1 + p.n_keys + c, p.icol[c], r, li);
-        const unsigned long long a = v < 0 ? 0ull - (unsigned long long)v : (unsigned long long)v;
-        maxabs = a > maxabs ? a : maxabs;
-        big |= a >= (1ull << 26);
-        sival[c * TS + pos] = v;
-        si32[c * TS + pos] = (int)v;
-      }
-#pragma unroll
-      for (int c = 0; c < NF; ++c) {
-        const double v = __longlong_as_double(
-            (long long)raw_u64(p, rt, 1 + p.n_keys + p.ni + c, p.fcol[c], r, li));
-        nonfin |= !finite_bits(v);
-        sfval[c * TS + pos] = v;
-      }
-      if (MM) smval[pos] = __longlong_as_double((long long)raw_u64(p, rt, 1 + p.n_keys + p.ni + p.nf,
-                                                                   p.mcol, r, li));
-    };
-    auto push_queue = [&](bool pending, int pos, int li) {
-      const unsigned pm = __ballot_sync(0xffffffffu, pending);
-      int qb = 0;
-      if (lane == 0 && pm) qb = atomicAdd(&misc->nqueue, __popc(pm));
-      qb = __shfl_sync(0xffffffffu, qb, 0) + __popc(pm & lt_mask);
-      if (pending) {
-        qpos[qb] = (unsigned short)pos;
-        qrow[qb] = (unsigned short)li;
-      }
-    };
-    for (int la = tid; la < T; la += 2 * nth) {
-      const int lb = la + nth;  // T is a multiple of 2 * nth
-      const unsigned short sa = sslot[la], sb = sslot[lb];
-      const int pa = sa != kNone ? ucnt[(la >> 5) * Lcap + sa] + srank[la] : 0;
-      const int pb = sb != kNone ? ucnt[(lb >> 5) * Lcap + sb] + srank[lb] : 0;
-      bool qa = false, qb = false;
-      if (p.mask_in) {
-        if (sa != kNone) smask[pa] = raw_u64(p, rt, 0, p.mask_in, base + la, la);
-        if (sb != kNone) smask[pb] = raw_u64(p, rt, 0, p.mask_in, base + lb, lb);
-      } else {
-        const uint64_t ka = sa != kNone ? raw_u64(p, rt, 0, p.pu_key, base + la, la) : 0ull;
-        const uint64_t kb = sb != kNone ? raw_u64(p, rt, 0, p.pu_key, base + lb, lb) : 0ull;
-        HashState ha, hb;
-        pac_hash_begin2(ka, kb, p.salt, ha, hb);
-        if (sa != kNone) {
-          smask[pa] = ha.x ^ (((__popcll(ha.x) > 32) ? ha.x : ~ha.x) ^ ha.cand);
-          qa = ha.k > 0;
-        }
-        if (sb != kNone) {
-          smask[pb] = hb.x ^ (((__popcll(hb.x) > 32) ? hb.x : ~hb.x) ^ hb.cand);
-          qb = hb.k > 0;
-        }
-      }
-      if (sa != kNone) stage_values(la, pa);
-      if (sb != kNone) stage_values(lb, pb);
-      push_queue(qa, pa, la);
-      push_queue(qb, pb, lb);
-    }
-    if (NI > 0 && __any_sync(0xffffffffu, big) && lane == 0) misc->big = 1;
-    if (NF > 0 && __any_sync(0xffffffffu, nonfin) && lane == 0) misc->nonfinite = 1;
-    __syncthreads();
-
-    // ---------------- A3: finish the queued masks.  State re-derived from the key and the
-    // partial mask: cand = majority positions of the current word, k = |popcount - 32|.
-    // One extra draw word for every queued row (branch-free), then a loop for the few left.
-    {
-      const int qn = misc->nqueue;
-      for (int qi = tid; qi < qn; qi += nth) {
-        const int pos = qpos[qi];
-        const int li = qrow[qi];
-        const uint64_t x = fmix64(raw_u64(p, rt, 0, p.pu_key, base + li, li) ^ p.salt);
-        const uint64_t m = smask[pos];
-        smask[pos] = pac_hash_finish(x, (__popcll(x) > 32) ? m : ~m, abs(__popcll(m) - 32));
-      }
-    }
-    __syncthreads();
+    if (staged) tile_front<NI, NF, MM, true>(p, sm, L, base, tn, maxabs);
+    else tile_front<NI, NF, MM, false>(p, sm, L, base, tn, maxabs);
     // the raw tile buffer is free: stage the next tile while phase C runs
     if (tid == 0 && staged_tile(tile + 1)) issue_tile(p, raw, mbar, (tile + 1) * T, T);
 
     // ---------------- C: world-parallel runs, transposed "Four Russians" tables
-    {
+    if (!(p.ablate & 4)) {
       RunCtx x;
-      x.smask = smask;
-      x.sival = sival;
-      x.si32 = si32;
-      x.sfval = sfval;
-      x.smval = smval;
-      x.hist = hist;
-      x.offs = offs;
-      x.runoffs = runoffs;
-      x.tcs = tcs;
-      x.TS = TS;
+      x.smask = sm.smask;
+      x.sival = sm.sival;
+      x.si32 = sm.si32;
+      x.sfval = sm.sfval;
+      x.smval = sm.smval;
+      x.hist = sm.hist;
+      x.offs = sm.offs;
+      x.runoffs = sm.runoffs;
+      x.tcs = sm.tcs;
+      x.TS = L.TS;
       x.Lcap = Lcap;
       x.R = misc->nruns;
       const bool small = (NI == 0) || misc->big == 0;
       const bool fin = (NF == 0) || misc->nonfinite == 0;
-      if (small && fin) run_tiles<NI, NF, MM, true, true>(acc, x, cnt, isum, fsum, emin, emax, wid, nw, lane);
-      else if (small) run_tiles<NI, NF, MM, true, false>(acc, x, cnt, isum, fsum, emin, emax, wid, nw, lane);
-      else if (fin) run_tiles<NI, NF, MM, false, true>(acc, x, cnt, isum, fsum, emin, emax, wid, nw, lane);
-      else run_tiles<NI, NF, MM, false, false>(acc, x, cnt, isum, fsum, emin, emax, wid, nw, lane);
+      if (small && fin)
+        run_tiles<NI, NF, MM, true, true>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
+      else if (small)
+        run_tiles<NI, NF, MM, true, false>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
+      else if (fin)
+        run_tiles<NI, NF, MM, false, true>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
+      else
+        run_tiles<NI, NF, MM, false, false>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
     }
     __syncthreads();
   }
-  acc.flush(cnt, isum, fsum, emin, emax, Lcap, lane);
+  acc.flush(sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, Lcap, lane);
   __syncthreads();
 
   // ---------------- CTA table -> provisional HBM table
@@ -807,25 +853,25 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLa
   if (tid == 0) atomicMax(&p.dbg[1], (unsigned long long)misc->nlocal);
   for (int i = tid; i < nloc * kM; i += nth) {
     const int s = i / kM;
-    const int prov = lprov[s];
+    const int prov = sm.lprov[s];
     if (prov < 0) continue;
     const size_t g = (size_t)prov * kM + (i % kM);
-    if (cnt[i]) atomicAdd(&p.prov_count[g], (unsigned long long)cnt[i]);
+    if (sm.cnt[i]) atomicAdd(&p.prov_count[g], (unsigned long long)sm.cnt[i]);
 #pragma unroll
     for (int c = 0; c < NI; ++c) {
-      const unsigned long long v = isum[(size_t)c * Lcap * kM + i];
+      const unsigned long long v = sm.isum[(size_t)c * Lcap * kM + i];
       if (v) atomicAdd(&p.prov_isum[c][g], v);
     }
 #pragma unroll
     for (int c = 0; c < NF; ++c) {
-      const double v = fsum[(size_t)c * Lcap * kM + i];
+      const double v = sm.fsum[(size_t)c * Lcap * kM + i];
       if (v != 0.0) atomicAdd(&p.prov_fsum[c][g], v);
     }
-    if (MM & 1) atomicMin(&p.prov_min[g], emin[i]);
-    if (MM & 2) atomicMax(&p.prov_max[g], emax[i]);
+    if (MM & 1) atomicMin(&p.prov_min[g], sm.emin[i]);
+    if (MM & 2) atomicMax(&p.prov_max[g], sm.emax[i]);
   }
   for (int s = tid; s < nloc; s += nth)
-    if (lprov[s] >= 0 && lrows[s]) atomicAdd(&p.prov_rows[lprov[s]], lrows[s]);
+    if (sm.lprov[s] >= 0 && sm.lrows[s]) atomicAdd(&p.prov_rows[sm.lprov[s]], sm.lrows[s]);
   if (NI > 0) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -1548,14 +1594,15 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
         };
         p.nraw = 0;
         add(d_mask ? (const void*)d_mask : (const void*)d_pu_key, 8);
-        for (int c = 0; c < n_keys; ++c) add(keys[c].d_col, keys[c].elem_bytes);
         for (int c = 0; c < A.ni; ++c) add(A.icol[c], 8);
         for (int c = 0; c < A.nf; ++c) add(A.fcol[c], 8);
         if (A.has_min || A.has_max) add(A.mcol, 8);
+        for (int c = 0; c < n_keys; ++c) add(keys[c].d_col, keys[c].elem_bytes);
         int copied = 0;
         for (int i = 0; i < p.nraw; ++i) copied += L.T * p.raw_eb[i];
         p.raw_bytes = copied;
         p.tma_ok = (aligned && !getenv("PAC_NO_TMA")) ? 1 : 0;
+        p.ablate = getenv("PAC_ABLATE") ? atoi(getenv("PAC_ABLATE")) : 0;
       }
       if (getenv("PAC_DEBUG"))
         fprintf(stderr, "[libpac] k_agg_tiles<%d,%d,%d> T=%d Lcap=%d LH=%d smem=%d B (G_cap=%lld)\n", A.ni,
