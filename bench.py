@@ -203,7 +203,7 @@ def main():
     vals = [None if i < 0 else cols["values"][i] for _, i in w.aggs]
     kinds = [k for k, _ in w.aggs]
     # capacity hints from the key domains of the synthetic configs (R20 packed keys)
-    G_cap = {"C1": 1, "C2": 16, "C4": 1024, "C5": 128}.get(w.name, 1 << 21)
+    G_cap = {"C1": 1, "C2": 8, "C4": 1024, "C5": 100}.get(w.name, 1 << 21)
     seed = 0x5EED
     sess = pac.Session(seed, w.budget)
     ag = pac.Aggregator(kinds, G_cap, dev)

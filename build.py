@@ -16,8 +16,7 @@ import sys
 ROOT = os.path.dirname(os.path.abspath(__file__))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-           "-Xptxas", "-v"]
+NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 TARGETS = {
     "libpac": (os.path.join(ROOT, "paper_2603_15023_b200", "libpac.so"),
@@ -37,15 +36,33 @@ def _stale(out, deps):
 
 
 def build_cuda(name: str, force: bool = False, verbose: bool = False) -> str:
+    """Compile every .cu of the target to an object in parallel, then link the .so."""
     out, srcs, hdrs = TARGETS[name]
-    if force or _stale(out, srcs + hdrs):
-        cmd = [NVCC] + ARCH + NVFLAGS + ["-I", os.path.join(ROOT, "include"), "-o", out] + srcs
+    if not (force or _stale(out, srcs + hdrs)):
+        return out
+    objdir = os.path.join(ROOT, "build", name)
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC] + ARCH + NVFLAGS + ["-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]
         r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, r
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        results = list(ex.map(compile_one, srcs))
+    for src, obj, r in results:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed for {name}")
+            raise RuntimeError(f"nvcc failed for {src}")
         if verbose:
             sys.stderr.write(r.stderr)
+    cmd = [NVCC] + ARCH + ["-shared", "-o", out] + [o for _, o, _ in results]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"link failed for {name}")
     return out
 
 

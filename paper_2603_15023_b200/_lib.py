@@ -5,7 +5,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpac.so")
+LIB_PATH = os.environ.get("PAC_LIB") or os.path.join(HERE, "libpac.so")  # PAC_LIB: A/B experiments
 
 PAC_M = 64
 PAC_MAX_AGGS = 8

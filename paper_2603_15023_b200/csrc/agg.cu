@@ -18,188 +18,9 @@
 #include <cstdlib>
 #include <vector>
 
-#include "common.cuh"
+#include "agg_tiles.cuh"
 
 namespace pac {
-
-constexpr int kThreads = 512;      // k_agg_minmax
-constexpr int kTileThreads = 256;  // k_agg_tiles: 128-register budget (2 CTAs / SM)
-constexpr int kOvfBase = 0x20000000;  // local-dict code for keys without a local slot
-constexpr int kSmallSort = 4096;      // single-CTA bitonic sort up to this many groups
-
-struct AggPlan {
-  int64_t n_rows;
-  const long long* pu_key;
-  const unsigned long long* mask_in;
-  uint64_t salt;
-  int n_keys;
-  const void* key_col[PAC_MAX_KEYS];
-  int key_bytes[PAC_MAX_KEYS];
-  int ni, nf, has_min, has_max, has_count;
-  const long long* icol[2];
-  const double* fcol[2];
-  const double* mcol;
-  // HBM dictionary + provisional table (workspace)
-  unsigned long long* gkey;
-  int* gstate;
-  uint32_t hmask;
-  int* gcounter;
-  unsigned long long* gmaxabs;  // max |v| over int64 sum columns (overflow check)
-  unsigned long long* dbg;      // [0] rows sent to the HBM tier, [1] max local slots used
-  // raw input columns staged per tile by 1-D TMA bulk copies (k_agg_tiles):
-  // 0 = pu_key or mask, 1..n_keys = key columns, then int64 sums, f64 sums, min/max column
-  int nraw, tma_ok;
-  int ablate;  // profiling only (PAC_ABLATE): 1 = no draws, 2 = no A3, 4 = no phase C
-  const void* raw_src[1 + PAC_MAX_KEYS + 5];
-  int raw_eb[1 + PAC_MAX_KEYS + 5];
-  int raw_off[1 + PAC_MAX_KEYS + 5];  // byte offset of the column inside the raw tile buffer
-  int raw_bytes;                       // bytes of one staged tile
-  int64_t G_cap;
-  unsigned long long* prov_key;
-  unsigned long long* prov_rows;
-  unsigned long long* prov_count;
-  unsigned long long* prov_isum[2];
-  double* prov_fsum[2];
-  long long* prov_min;
-  long long* prov_max;
-};
-
-struct SmemLayout {
-  int T, TS, Lcap, LH;
-  int o_lkey, o_lstate, o_lprov, o_lrows, o_cnt, o_isum, o_fsum, o_min, o_max;
-  int o_mask, o_slot, o_rank, o_ucnt, o_queue, o_ival, o_i32, o_fval, o_mval, o_hist, o_offs,
-      o_runoffs, o_tcs, o_raw, o_mbar, o_misc;
-  int bytes;
-};
-
-struct Misc {
-  int nlocal;   // local slots handed out
-  int ndict;    // local dictionary reservations
-  int nruns;    // runs in the current tile
-  int big;        // some int64 value of the tile has |v| >= 2^26 (no int32 tables)
-  int nqueue;     // rows whose mask needs more than one draw word
-  int nonfinite;  // some f64 value of the tile is inf/nan (no 0/1-FMA tables)
-  int pad[2];
-};
-
-// ------------------------------------------------------------------ dictionaries
-__device__ __forceinline__ void init_prov_slot(const AggPlan& p, int prov, uint64_t key) {
-  p.prov_key[prov] = key;
-  p.prov_rows[prov] = 0;
-  size_t b = (size_t)prov * kM;
-  for (int j = 0; j < kM; ++j) {
-    if (p.has_count) p.prov_count[b + j] = 0;
-    for (int c = 0; c < p.ni; ++c) p.prov_isum[c][b + j] = 0;
-    for (int c = 0; c < p.nf; ++c) p.prov_fsum[c][b + j] = 0.0;
-    if (p.has_min) p.prov_min[b + j] = kEncPosInf;
-    if (p.has_max) p.prov_max[b + j] = kEncNegInf;
-  }
-}
-
-// Insert-or-find `key` in the HBM dictionary; returns the provisional slot, or -1 when
-// the capacity G_cap is exhausted (the table is then flagged by the finish kernel).
-__device__ int global_slot(const AggPlan& p, uint64_t key) {
-  uint32_t h = dict_hash(key) & p.hmask;
-  for (;;) {
-    int st = *(volatile int*)&p.gstate[h];
-    if (st == 0) {
-      if (atomicCAS(&p.gstate[h], 0, -1) == 0) {
-        int prov = atomicAdd(p.gcounter, 1);
-        if (prov >= p.G_cap) {  // out of capacity: release the claim, report via counter
-          __threadfence();
-          atomicExch(&p.gstate[h], 0);
-          return -1;
-        }
-        *(volatile unsigned long long*)&p.gkey[h] = key;
-        init_prov_slot(p, prov, key);
-        __threadfence();
-        atomicExch(&p.gstate[h], prov + 1);
-        return prov;
-      }
-      continue;
-    }
-    if (st < 0) continue;  // being written
-    __threadfence();
-    if (*(volatile unsigned long long*)&p.gkey[h] == key) return st - 1;
-    h = (h + 1) & p.hmask;
-  }
-}
-
-// CTA-local dictionary: code = s+1 for local slot s (< Lcap); kOvfBase + prov + 1 for a
-// key that has no local slot (its rows go straight to the HBM table; prov -1 = dropped).
-// An empty entry is claimed with CAS first; only then is the entry counted, so concurrent
-// contenders for one key never inflate the fill count.  At half full no more keys are
-// inserted (their rows use the HBM dictionary directly).
-__device__ int local_code(const AggPlan& p, uint64_t key, unsigned long long* lkey, int* lstate,
-                          int LH, int* lprov, int Lcap, Misc* misc) {
-  uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 40) & (LH - 1);
-  for (;;) {
-    int st = *(volatile int*)&lstate[h];
-    if (st == 0) {
-      if (atomicCAS(&lstate[h], 0, -1) == 0) {
-        if (atomicAdd(&misc->ndict, 1) >= LH / 2) {  // too full: release, use the HBM tier
-          atomicSub(&misc->ndict, 1);
-          __threadfence_block();
-          atomicExch(&lstate[h], 0);
-          return kOvfBase + global_slot(p, key) + 1;
-        }
-        lkey[h] = key;
-        int s = atomicAdd(&misc->nlocal, 1);
-        int prov = global_slot(p, key);
-        int code;
-        if (s < Lcap) {
-          lprov[s] = prov;
-          code = s + 1;
-        } else {
-          code = kOvfBase + prov + 1;
-        }
-        __threadfence_block();
-        atomicExch(&lstate[h], code);
-        return code;
-      }
-      continue;
-    }
-    if (st < 0) continue;
-    __threadfence_block();
-    if (*(volatile unsigned long long*)&lkey[h] == key) return st;
-    h = (h + 1) & (LH - 1);
-  }
-}
-
-__device__ __forceinline__ uint64_t row_group_key(const AggPlan& p, int64_t r) {
-  uint64_t packed = 0;
-#pragma unroll
-  for (int c = 0; c < PAC_MAX_KEYS; ++c) {
-    if (c < p.n_keys) {
-      int w = p.key_bytes[c];
-      uint64_t v = load_key_part(p.key_col[c], w, r);
-      packed = (w == 8) ? v : ((packed << (8 * w)) | v);
-    }
-  }
-  return packed;
-}
-
-// Direct HBM update for a row whose group has no CTA-local slot.
-template <int NI, int NF, int MM>
-__device__ __forceinline__ void global_row_update(const AggPlan& p, int prov, uint64_t m,
-                                                  const long long (&iv)[NI > 0 ? NI : 1],
-                                                  const double (&fv)[NF > 0 ? NF : 1], double mv) {
-  atomicAdd(&p.dbg[0], 1ull);
-  if (prov < 0) return;
-  atomicAdd(&p.prov_rows[prov], 1ull);
-  const size_t b = (size_t)prov * kM;
-#pragma unroll 1
-  for (int j = 0; j < kM; ++j) {
-    if (!((m >> j) & 1ull)) continue;
-    atomicAdd(&p.prov_count[b + j], 1ull);
-#pragma unroll
-    for (int c = 0; c < NI; ++c) atomicAdd(&p.prov_isum[c][b + j], (unsigned long long)iv[c]);
-#pragma unroll
-    for (int c = 0; c < NF; ++c) atomicAdd(&p.prov_fsum[c][b + j], fv[c]);
-    if (MM & 1) atomicMin(&p.prov_min[b + j], enc_f64(mv));
-    if (MM & 2) atomicMax(&p.prov_max[b + j], enc_f64(mv));
-  }
-}
 
 // ------------------------------------------------------------------ k_mask
 __global__ void __launch_bounds__(256) k_mask(const long long* __restrict__ key, int64_t n,
@@ -207,679 +28,6 @@ __global__ void __launch_bounds__(256) k_mask(const long long* __restrict__ key,
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     out[i] = pac_hash_dev((uint64_t)__ldg(key + i), salt);
-}
-
-// ------------------------------------------------------------------ TMA bulk staging
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* m, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* m) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P1;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      " @!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(m)), "r"(parity) : "memory");
-}
-// one thread: stage the raw columns of the full tile starting at row `base`
-__device__ __forceinline__ void issue_tile(const AggPlan& p, unsigned char* raw, unsigned long long* mbar,
-                                           int64_t base, int T) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  mbar_expect_tx(mbar, (uint32_t)p.raw_bytes);
-  for (int i = 0; i < p.nraw; ++i)
-    bulk_g2s(raw + p.raw_off[i], (const char*)p.raw_src[i] + base * p.raw_eb[i], (uint32_t)(T * p.raw_eb[i]), mbar);
-}
-
-// ------------------------------------------------------------------ k_agg_tiles (v3)
-// Bit-matrix transpose of a 32-row run: on input lane r holds row r's
-// 32-bit mask word; on output lane c holds the pattern of world c over the run.  Stage s
-// swaps the off-diagonal s x s blocks: the partner's word is rotated by s (low lane) or
-// 32-s (high lane) with one funnel shift and merged with one LOP3 under a per-lane mask.
-// Per-lane constants of the 5 stages live in shared memory (tcs[stage*32 + lane] =
-// {keep mask, rotate amount}), loaded once per run: cheaper than rematerialising them.
-__device__ __forceinline__ uint2 transpose_const(int lane, int i) {
-  const int s = 16 >> i;
-  const uint32_t M = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
-                   : s == 2 ? 0x33333333u : 0x55555555u;
-  const bool up = (lane & s) != 0;
-  return make_uint2(up ? ~M : M, (uint32_t)(up ? 32 - s : s));
-}
-
-__device__ __forceinline__ void transpose2x32(uint32_t& a, uint32_t& b, const uint2* __restrict__ tcs,
-                                              int lane) {
-  uint2 c[5];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) c[i] = tcs[i * 32 + lane];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    const int s = 16 >> i;
-    const uint32_t ya = __shfl_xor_sync(0xffffffffu, a, s);
-    const uint32_t yb = __shfl_xor_sync(0xffffffffu, b, s);
-    a = (a & c[i].x) | (__funnelshift_l(ya, ya, c[i].y) & ~c[i].x);
-    b = (b & c[i].x) | (__funnelshift_l(yb, yb, c[i].y) & ~c[i].x);
-  }
-}
-
-__device__ __forceinline__ double shfl_d(double v, int src) {
-  const int lo = __shfl_sync(0xffffffffu, __double2loint(v), src);
-  const int hi = __shfl_sync(0xffffffffu, __double2hiint(v), src);
-  return __hiloint2double(hi, lo);
-}
-
-__device__ __forceinline__ bool finite_bits(double v) {
-  return (__double2hiint(v) & 0x7FF00000) != 0x7FF00000;
-}
-
-// Register accumulators of the slot a warp is currently working on (lane: worlds lane, lane+32).
-template <int NI, int NF, int MM>
-struct WarpAcc {
-  int cur;
-  unsigned c0, c1;
-  long long ia0[NI > 0 ? NI : 1], ia1[NI > 0 ? NI : 1];
-  double fa0[NF > 0 ? NF : 1], fa1[NF > 0 ? NF : 1];
-  double mn0, mn1, mx0, mx1;
-
-  __device__ __forceinline__ void reset() {
-    c0 = c1 = 0;
-#pragma unroll
-    for (int c = 0; c < NI; ++c) ia0[c] = ia1[c] = 0;
-#pragma unroll
-    for (int c = 0; c < NF; ++c) fa0[c] = fa1[c] = 0.0;
-    mn0 = mn1 = INFINITY;
-    mx0 = mx1 = -INFINITY;
-  }
-  // add into the CTA's smem table (shared by the warps working on the same slot)
-  __device__ __forceinline__ void flush(unsigned* cnt, unsigned long long* isum, double* fsum, long long* emin,
-                                        long long* emax, int Lcap, int lane) {
-    if (cur < 0) return;
-    const size_t b = (size_t)cur * kM;
-    if (c0) atomicAdd(&cnt[b + lane], c0);
-    if (c1) atomicAdd(&cnt[b + lane + 32], c1);
-#pragma unroll
-    for (int c = 0; c < NI; ++c) {
-      atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane], (unsigned long long)ia0[c]);
-      atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane + 32], (unsigned long long)ia1[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < NF; ++c) {
-      atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane], fa0[c]);
-      atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane + 32], fa1[c]);
-    }
-    if (MM & 1) {
-      atomicMin(&emin[b + lane], enc_f64(mn0));
-      atomicMin(&emin[b + lane + 32], enc_f64(mn1));
-    }
-    if (MM & 2) {
-      atomicMax(&emax[b + lane], enc_f64(mx0));
-      atomicMax(&emax[b + lane + 32], enc_f64(mx1));
-    }
-    reset();
-  }
-};
-
-struct RunCtx {  // read-only per-tile state of phase C
-  const unsigned long long* smask;
-  const long long* sival;
-  const int* si32;
-  const double* sfval;
-  const double* smval;
-  const int* hist;
-  const int* offs;
-  const int* runoffs;
-  const uint2* tcs;
-  int TS, Lcap, R;
-};
-
-// Phase C of one tile for one warp: runs [r0, r1) of the tile's slot-sorted rows.
-// SMALL: int64 values of the tile fit int32 nibble tables; FIN: f64 values are finite, so
-// the f64 nibble tables are built with exact 0/1 FMAs.
-template <int NI, int NF, int MM, bool SMALL, bool FIN>
-__device__ __forceinline__ void run_tiles(WarpAcc<NI, NF, MM>& acc, const RunCtx& x, unsigned* cnt,
-                                          unsigned long long* isum, double* fsum, long long* emin,
-                                          long long* emax, int wid, int nw, int lane) {
-  const int R = x.R, TS = x.TS;
-  const int r0 = (int)(((long long)R * wid) / nw);
-  const int r1 = (int)(((long long)R * (wid + 1)) / nw);
-  if (r0 >= r1) return;
-  const int sub = lane & 15;
-  const int tsrc = (lane >> 4) << 2;
-  const int ib0 = sub & 1, ib1 = (sub >> 1) & 1, ib2 = (sub >> 2) & 1, ib3 = (sub >> 3) & 1;
-  const double db0 = ib0, db1 = ib1, db2 = ib2, db3 = ib3;
-  int s;
-  {
-    int lo = 0, hi = x.Lcap;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (x.runoffs[mid] <= r0) lo = mid; else hi = mid - 1;
-    }
-    s = lo;
-  }
-  int rs_end = x.runoffs[s + 1];
-  int k0 = 32 * (r0 - x.runoffs[s]);
-  int slot_beg = x.offs[s], slot_len = x.hist[s];
-  for (int r = r0; r < r1; ++r) {
-    if (r >= rs_end) {  // next non-empty slot
-      do {
-        ++s;
-        rs_end = x.runoffs[s + 1];
-      } while (rs_end <= r);
-      k0 = 0;
-      slot_beg = x.offs[s];
-      slot_len = x.hist[s];
-    }
-    if (s != acc.cur) {
-      acc.flush(cnt, isum, fsum, emin, emax, x.Lcap, lane);
-      acc.cur = s;
-    }
-    const int beg = slot_beg + k0;
-    const int len = min(32, slot_len - k0);
-    k0 += 32;
-    const uint64_t m = lane < len ? x.smask[beg + lane] : 0ull;
-    uint32_t P = (uint32_t)m, Q = (uint32_t)(m >> 32);
-    transpose2x32(P, Q, x.tcs, lane);
-    acc.c0 += __popc(P);
-    acc.c1 += __popc(Q);
-    // nibble indices: table A (lanes 0-15) covers rows 8q..8q+3, B (16-31) rows 8q+4..8q+7;
-    // shfl uses only the low 5 bits of the source lane.
-    const uint32_t PA = P & 0x0F0F0F0Fu, PB = ((P >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
-    const uint32_t QA = Q & 0x0F0F0F0Fu, QB = ((Q >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
-    const int nq = (len + 7) >> 3;
-    int rs0[NI > 0 ? NI : 1], rs1[NI > 0 ? NI : 1];
-#pragma unroll
-    for (int c = 0; c < NI; ++c) rs0[c] = rs1[c] = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (q >= nq) break;
-      const int a0 = (int)(PA >> (8 * q)), b0 = (int)(PB >> (8 * q));
-      const int a1 = (int)(QA >> (8 * q)), b1 = (int)(QB >> (8 * q));
-      const int row = beg + 8 * q + tsrc;
-#pragma unroll
-      for (int c = 0; c < NI; ++c) {
-        if (SMALL) {
-          const int4 v = *(const int4*)(x.si32 + c * TS + row);
-          const int t = v.x * ib0 + v.y * ib1 + v.z * ib2 + v.w * ib3;
-          rs0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
-          rs1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
-        } else {
-          const longlong2 u = *(const longlong2*)(x.sival + c * TS + row);
-          const longlong2 w = *(const longlong2*)(x.sival + c * TS + row + 2);
-          const long long t = u.x * ib0 + u.y * ib1 + w.x * ib2 + w.y * ib3;
-          acc.ia0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
-          acc.ia1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < NF; ++c) {
-        const double2 u = *(const double2*)(x.sfval + c * TS + row);
-        const double2 w = *(const double2*)(x.sfval + c * TS + row + 2);
-        double t;
-        if (FIN) {  // exact: 0*v + t == t and 1*v + t == v + t for finite v
-          t = fma(db3, w.y, fma(db2, w.x, fma(db1, u.y, db0 * u.x)));
-        } else {
-          t = ib0 ? u.x : 0.0;
-          if (ib1) t += u.y;
-          if (ib2) t += w.x;
-          if (ib3) t += w.y;
-        }
-        acc.fa0[c] += shfl_d(t, a0);
-        acc.fa0[c] += shfl_d(t, b0);
-        acc.fa1[c] += shfl_d(t, a1);
-        acc.fa1[c] += shfl_d(t, b1);
-      }
-      if (MM) {
-        const double2 u = *(const double2*)(x.smval + row);
-        const double2 w = *(const double2*)(x.smval + row + 2);
-        if (MM & 1) {
-          double t = ib0 ? u.x : INFINITY;
-          if (ib1) t = fmin(t, u.y);
-          if (ib2) t = fmin(t, w.x);
-          if (ib3) t = fmin(t, w.y);
-          acc.mn0 = fmin(acc.mn0, fmin(shfl_d(t, a0), shfl_d(t, b0)));
-          acc.mn1 = fmin(acc.mn1, fmin(shfl_d(t, a1), shfl_d(t, b1)));
-        }
-        if (MM & 2) {
-          double t = ib0 ? u.x : -INFINITY;
-          if (ib1) t = fmax(t, u.y);
-          if (ib2) t = fmax(t, w.x);
-          if (ib3) t = fmax(t, w.y);
-          acc.mx0 = fmax(acc.mx0, fmax(shfl_d(t, a0), shfl_d(t, b0)));
-          acc.mx1 = fmax(acc.mx1, fmax(shfl_d(t, a1), shfl_d(t, b1)));
-        }
-      }
-    }
-    if (SMALL) {
-#pragma unroll
-      for (int c = 0; c < NI; ++c) {
-        acc.ia0[c] += rs0[c];
-        acc.ia1[c] += rs1[c];
-      }
-    }
-  }
-}
-
-struct TileSmem {
-  unsigned long long* lkey;
-  int* lstate;
-  int* lprov;
-  unsigned long long* lrows;
-  unsigned* cnt;
-  unsigned long long* isum;
-  double* fsum;
-  long long* emin;
-  long long* emax;
-  unsigned long long* smask;  // [TS] slot-sorted masks
-  long long* sival;           // [NI][TS]
-  int* si32;                  // [NI][TS]
-  double* sfval;              // [NF][TS]
-  double* smval;              // [TS]
-  unsigned short* sslot;      // [T]
-  unsigned char* srank;       // [T]
-  unsigned short* ucnt;       // [units][Lcap]
-  unsigned short* qpos;       // [T]
-  unsigned short* qrow;       // [T]
-  int* hist;
-  int* offs;
-  int* runoffs;
-  uint2* tcs;
-  Misc* misc;
-  const unsigned char* raw;   // staged raw tile: 8-byte columns k at k*T*8, then key columns
-};
-
-// Column k of the tile: 0 = pu_key/mask, 1..NI int64 sums, NI+1..NI+NF f64 sums, then the
-// MIN/MAX column; group-key columns after them.  Staged tiles read the TMA copy in smem.
-template <bool STAGED>
-struct TileCols {
-  const AggPlan* p;
-  const unsigned char* raw;
-  int64_t base;
-  int T;
-  __device__ __forceinline__ uint64_t w8(int k, int li) const {
-    if (STAGED) return ((const unsigned long long*)raw)[(size_t)k * T + li];
-    return (uint64_t)__ldg((const unsigned long long*)p->raw_src[k] + base + li);
-  }
-  __device__ __forceinline__ uint64_t group_key(int k0, int li) const {
-    uint64_t packed = 0;
-#pragma unroll
-    for (int c = 0; c < PAC_MAX_KEYS; ++c) {
-      if (c < p->n_keys) {
-        const int w = p->key_bytes[c];
-        uint64_t v;
-        if (STAGED) {
-          const unsigned char* col = raw + p->raw_off[k0 + c];
-          if (w == 1) v = col[li];
-          else if (w == 2) v = ((const unsigned short*)col)[li];
-          else if (w == 4) v = ((const unsigned*)col)[li];
-          else v = ((const unsigned long long*)col)[li];
-          v ^= 1ull << (8 * w - 1);
-        } else {
-          v = load_key_part(p->key_col[c], w, base + li);
-        }
-        packed = (w == 8) ? v : ((packed << (8 * w)) | v);
-      }
-    }
-    return packed;
-  }
-};
-
-// A1 (slots + ranks), B (offsets), A2 (hash word 0 + sorted staging), A3 (stragglers) of one
-// tile.  Leaves the slot-sorted tile in smem and the run table for phase C.
-template <int NI, int NF, int MM, bool STAGED>
-__device__ __forceinline__ void tile_front(const AggPlan& p, const TileSmem& sm, const SmemLayout& L, int64_t base,
-                                           int tn, unsigned long long& maxabs) {
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int lane = tid & 31, wid = tid >> 5;
-  const int T = L.T, TS = L.TS, Lcap = L.Lcap, LH = L.LH;
-  const int units = T >> 5;
-  const unsigned short kNone = 0xFFFF;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  constexpr int KF = 1 + NI;             // first f64 sum column
-  constexpr int KM = 1 + NI + NF;        // min/max column
-  constexpr int KK = 1 + NI + NF + (MM ? 1 : 0);  // first group-key column
-  TileCols<STAGED> tc{&p, sm.raw, base, T};
-  Misc* misc = sm.misc;
-
-  // ---------------- A1: group slot of every row + rank within its 32-row unit
-  for (int li = tid; li < T; li += nth) {
-    int s = -1;
-    if (li < tn) {
-      bool keep = true;
-      if (p.mask_in) keep = tc.w8(0, li) != 0ull;  // R21: a row in no world is dropped
-      if (keep) {
-        const uint64_t key = tc.group_key(KK, li);
-        const int code = local_code(p, key, sm.lkey, sm.lstate, LH, sm.lprov, Lcap, misc);
-        if (code < kOvfBase) {
-          s = code - 1;
-        } else {  // no local slot: straight to the HBM table (rare)
-          long long iv[NI > 0 ? NI : 1];
-          double fv[NF > 0 ? NF : 1];
-#pragma unroll
-          for (int c = 0; c < NI; ++c) iv[c] = (long long)tc.w8(1 + c, li);
-#pragma unroll
-          for (int c = 0; c < NF; ++c) fv[c] = __longlong_as_double((long long)tc.w8(KF + c, li));
-          const double mv = MM ? __longlong_as_double((long long)tc.w8(KM, li)) : 0.0;
-          const uint64_t m = p.mask_in ? tc.w8(0, li) : pac_hash_dev(tc.w8(0, li), p.salt);
-          global_row_update<NI, NF, MM>(p, code - kOvfBase - 1, m, iv, fv, mv);
-        }
-      }
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, s >= 0 ? (unsigned)s : 0x10000u + lane);
-    if (s >= 0) {
-      sm.srank[li] = (unsigned char)__popc(peers & lt_mask);
-      if ((peers & lt_mask) == 0) sm.ucnt[(li >> 5) * Lcap + s] = (unsigned short)__popc(peers);
-    }
-    sm.sslot[li] = s >= 0 ? (unsigned short)s : kNone;
-  }
-  __syncthreads();
-
-  // ---------------- B: slot totals, 8-row padded offsets, run offsets, unit positions
-  for (int s = tid; s < Lcap; s += nth) {
-    int tot = 0;
-    for (int u = 0; u < units; ++u) tot += sm.ucnt[u * Lcap + s];
-    sm.hist[s] = tot;
-  }
-  __syncthreads();
-  if (wid == 0) {
-    const int per = (Lcap + 31) / 32;
-    const int s0 = lane * per;
-    int hsum = 0, rsum = 0;
-    for (int s = s0; s < min(Lcap, s0 + per); ++s) {
-      hsum += (sm.hist[s] + 7) & ~7;
-      rsum += (sm.hist[s] + 31) >> 5;
-    }
-    int hx = hsum, rx = rsum;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, hx, d);
-      const int b = __shfl_up_sync(0xffffffffu, rx, d);
-      if (lane >= d) {
-        hx += a;
-        rx += b;
-      }
-    }
-    hx -= hsum;
-    rx -= rsum;
-    for (int s = s0; s < min(Lcap, s0 + per); ++s) {
-      sm.offs[s] = hx;
-      sm.runoffs[s] = rx;
-      sm.lrows[s] += (unsigned long long)sm.hist[s];
-      hx += (sm.hist[s] + 7) & ~7;
-      rx += (sm.hist[s] + 31) >> 5;
-    }
-    if (lane == 31) {
-      sm.runoffs[Lcap] = rx;
-      misc->nruns = rx;
-    }
-  }
-  __syncthreads();
-  for (int s = tid; s < Lcap; s += nth) {
-    const int o0 = sm.offs[s];
-    int o = o0;
-    for (int u = 0; u < units; ++u) {
-      const int c = sm.ucnt[u * Lcap + s];
-      sm.ucnt[u * Lcap + s] = (unsigned short)o;
-      o += c;
-    }
-    for (int q = o; q < o0 + ((sm.hist[s] + 7) & ~7); ++q) {  // zero padding rows (mask 0)
-      sm.smask[q] = 0;
-#pragma unroll
-      for (int c = 0; c < NI; ++c) {
-        sm.sival[c * TS + q] = 0;
-        sm.si32[c * TS + q] = 0;
-      }
-#pragma unroll
-      for (int c = 0; c < NF; ++c) sm.sfval[c * TS + q] = 0.0;
-      if (MM) sm.smval[q] = 0.0;
-    }
-  }
-  __syncthreads();
-
-  // ---------------- A2: hash word 0 (two rows per thread, interleaved) + values, written
-  // straight to the slot-sorted position; rows still needing flips are queued for A3.
-  bool big = false, nonfin = false;
-  for (int la = tid; la < T; la += 2 * nth) {
-    const int lb = la + nth;  // T is a multiple of 2 * nth
-    const unsigned short sa = sm.sslot[la], sb = sm.sslot[lb];
-    const int pa = sa != kNone ? sm.ucnt[(la >> 5) * Lcap + sa] + sm.srank[la] : 0;
-    const int pb = sb != kNone ? sm.ucnt[(lb >> 5) * Lcap + sb] + sm.srank[lb] : 0;
-    bool qa = false, qb = false;
-    const uint64_t ka = sa != kNone ? tc.w8(0, la) : 0ull;
-    const uint64_t kb = sb != kNone ? tc.w8(0, lb) : 0ull;
-    uint64_t ma = ka, mb = kb;
-    if (!p.mask_in) {
-      HashState ha, hb;
-      if (p.ablate & 1) {
-        ha.x = ka; ha.cand = ka; ha.k = 0; hb.x = kb; hb.cand = kb; hb.k = 0;
-      } else {
-        pac_hash_begin2(ka, kb, p.salt, ha, hb);
-      }
-      ma = ha.x ^ (((__popcll(ha.x) > 32) ? ha.x : ~ha.x) ^ ha.cand);
-      mb = hb.x ^ (((__popcll(hb.x) > 32) ? hb.x : ~hb.x) ^ hb.cand);
-      qa = sa != kNone && ha.k > 0;
-      qb = sb != kNone && hb.k > 0;
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int li = h ? lb : la;
-      const int pos = h ? pb : pa;
-      if ((h ? sb : sa) == kNone) continue;
-      sm.smask[pos] = h ? mb : ma;
-#pragma unroll
-      for (int c = 0; c < NI; ++c) {
-        const long long v = (long long)tc.w8(1 + c, li);
-        const unsigned long long a = v < 0 ? 0ull - (unsigned long long)v : (unsigned long long)v;
-        maxabs = a > maxabs ? a : maxabs;
-        big |= a >= (1ull << 26);
-        sm.sival[c * TS + pos] = v;
-        sm.si32[c * TS + pos] = (int)v;
-      }
-#pragma unroll
-      for (int c = 0; c < NF; ++c) {
-        const double v = __longlong_as_double((long long)tc.w8(KF + c, li));
-        nonfin |= !finite_bits(v);
-        sm.sfval[c * TS + pos] = v;
-      }
-      if (MM) sm.smval[pos] = __longlong_as_double((long long)tc.w8(KM, li));
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const bool pend = h ? qb : qa;
-      const unsigned pm = __ballot_sync(0xffffffffu, pend);
-      int qbase = 0;
-      if (lane == 0 && pm) qbase = atomicAdd(&misc->nqueue, __popc(pm));
-      qbase = __shfl_sync(0xffffffffu, qbase, 0) + __popc(pm & lt_mask);
-      if (pend) {
-        sm.qpos[qbase] = (unsigned short)(h ? pb : pa);
-        sm.qrow[qbase] = (unsigned short)(h ? lb : la);
-      }
-    }
-  }
-  if (NI > 0 && __any_sync(0xffffffffu, big) && lane == 0) misc->big = 1;
-  if (NF > 0 && __any_sync(0xffffffffu, nonfin) && lane == 0) misc->nonfinite = 1;
-  __syncthreads();
-
-  // ---------------- A3: finish the queued masks.  State re-derived from the key and the
-  // partial mask: cand = majority positions of the current word, k = |popcount - 32|.
-  if (!(p.ablate & 2)) {
-    const int qn = misc->nqueue;
-    for (int qi = tid; qi < qn; qi += nth) {
-      const int pos = sm.qpos[qi];
-      const uint64_t x = fmix64(tc.w8(0, sm.qrow[qi]) ^ p.salt);
-      const uint64_t m = sm.smask[pos];
-      sm.smask[pos] = pac_hash_finish(x, (__popcll(x) > 32) ? m : ~m, abs(__popcll(m) - 32));
-    }
-  }
-  __syncthreads();
-}
-
-template <int NI, int NF, int MM>
-__global__ void __launch_bounds__(kTileThreads, 3) k_agg_tiles(AggPlan p, SmemLayout L) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  TileSmem sm;
-  sm.lkey = (unsigned long long*)(smem + L.o_lkey);
-  sm.lstate = (int*)(smem + L.o_lstate);
-  sm.lprov = (int*)(smem + L.o_lprov);
-  sm.lrows = (unsigned long long*)(smem + L.o_lrows);
-  sm.cnt = (unsigned*)(smem + L.o_cnt);
-  sm.isum = (unsigned long long*)(smem + L.o_isum);
-  sm.fsum = (double*)(smem + L.o_fsum);
-  sm.emin = (long long*)(smem + L.o_min);
-  sm.emax = (long long*)(smem + L.o_max);
-  sm.smask = (unsigned long long*)(smem + L.o_mask);
-  sm.sival = (long long*)(smem + L.o_ival);
-  sm.si32 = (int*)(smem + L.o_i32);
-  sm.sfval = (double*)(smem + L.o_fval);
-  sm.smval = (double*)(smem + L.o_mval);
-  sm.sslot = (unsigned short*)(smem + L.o_slot);
-  sm.srank = (unsigned char*)(smem + L.o_rank);
-  sm.ucnt = (unsigned short*)(smem + L.o_ucnt);
-  sm.qpos = (unsigned short*)(smem + L.o_queue);
-  sm.qrow = sm.qpos + L.T;
-  sm.hist = (int*)(smem + L.o_hist);
-  sm.offs = (int*)(smem + L.o_offs);
-  sm.runoffs = (int*)(smem + L.o_runoffs);
-  sm.tcs = (uint2*)(smem + L.o_tcs);
-  sm.misc = (Misc*)(smem + L.o_misc);
-  unsigned char* raw = smem + L.o_raw;
-  sm.raw = raw;
-  unsigned long long* mbar = (unsigned long long*)(smem + L.o_mbar);
-  Misc* misc = sm.misc;
-
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
-  const int T = L.T, Lcap = L.Lcap, LH = L.LH;
-  const int units = T >> 5;
-
-  for (int i = tid; i < LH; i += nth) sm.lstate[i] = 0;
-  for (int i = tid; i < Lcap; i += nth) sm.lrows[i] = 0;
-  for (int i = tid; i < Lcap * kM; i += nth) {
-    sm.cnt[i] = 0;
-#pragma unroll
-    for (int c = 0; c < NI; ++c) sm.isum[(size_t)c * Lcap * kM + i] = 0;
-#pragma unroll
-    for (int c = 0; c < NF; ++c) sm.fsum[(size_t)c * Lcap * kM + i] = 0.0;
-    if (MM & 1) sm.emin[i] = kEncPosInf;
-    if (MM & 2) sm.emax[i] = kEncNegInf;
-  }
-  if (tid < 32) {
-#pragma unroll
-    for (int i = 0; i < 5; ++i) sm.tcs[i * 32 + tid] = transpose_const(tid, i);
-  }
-  if (tid == 0) {
-    misc->nlocal = 0;
-    misc->ndict = 0;
-  }
-  unsigned long long maxabs = 0;
-
-  const int64_t ntiles = (p.n_rows + T - 1) / T;
-  const int64_t t_per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const int64_t t0 = (int64_t)blockIdx.x * t_per;
-  const int64_t t1 = min(ntiles, t0 + t_per);
-  // a tile is staged by TMA when it is full and every column is 16-byte aligned
-  auto staged_tile = [&](int64_t t) { return p.tma_ok && t < t1 && (t + 1) * T <= p.n_rows; };
-  uint32_t phase = 0;
-  if (tid == 0) {
-    mbar_init(mbar, 1);
-    if (staged_tile(t0)) issue_tile(p, raw, mbar, t0 * T, T);
-  }
-  __syncthreads();
-
-  WarpAcc<NI, NF, MM> acc;
-  acc.cur = -1;
-  acc.reset();
-
-  for (int64_t tile = t0; tile < t1; ++tile) {
-    const int64_t base = tile * T;
-    const int tn = (int)min((int64_t)T, p.n_rows - base);
-    for (int i = tid; i < units * Lcap; i += nth) sm.ucnt[i] = 0;
-    if (tid == 0) {
-      misc->big = 0;
-      misc->nonfinite = 0;
-      misc->nqueue = 0;
-    }
-    const bool staged = staged_tile(tile);
-    if (staged) {
-      mbar_wait(mbar, phase);
-      phase ^= 1u;
-    }
-    __syncthreads();
-    if (staged) tile_front<NI, NF, MM, true>(p, sm, L, base, tn, maxabs);
-    else tile_front<NI, NF, MM, false>(p, sm, L, base, tn, maxabs);
-    // the raw tile buffer is free: stage the next tile while phase C runs
-    if (tid == 0 && staged_tile(tile + 1)) issue_tile(p, raw, mbar, (tile + 1) * T, T);
-
-    // ---------------- C: world-parallel runs, transposed "Four Russians" tables
-    if (!(p.ablate & 4)) {
-      RunCtx x;
-      x.smask = sm.smask;
-      x.sival = sm.sival;
-      x.si32 = sm.si32;
-      x.sfval = sm.sfval;
-      x.smval = sm.smval;
-      x.hist = sm.hist;
-      x.offs = sm.offs;
-      x.runoffs = sm.runoffs;
-      x.tcs = sm.tcs;
-      x.TS = L.TS;
-      x.Lcap = Lcap;
-      x.R = misc->nruns;
-      const bool small = (NI == 0) || misc->big == 0;
-      const bool fin = (NF == 0) || misc->nonfinite == 0;
-      if (small && fin)
-        run_tiles<NI, NF, MM, true, true>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
-      else if (small)
-        run_tiles<NI, NF, MM, true, false>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
-      else if (fin)
-        run_tiles<NI, NF, MM, false, true>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
-      else
-        run_tiles<NI, NF, MM, false, false>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
-    }
-    __syncthreads();
-  }
-  acc.flush(sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, Lcap, lane);
-  __syncthreads();
-
-  // ---------------- CTA table -> provisional HBM table
-  const int nloc = min(misc->nlocal, Lcap);
-  if (tid == 0) atomicMax(&p.dbg[1], (unsigned long long)misc->nlocal);
-  for (int i = tid; i < nloc * kM; i += nth) {
-    const int s = i / kM;
-    const int prov = sm.lprov[s];
-    if (prov < 0) continue;
-    const size_t g = (size_t)prov * kM + (i % kM);
-    if (sm.cnt[i]) atomicAdd(&p.prov_count[g], (unsigned long long)sm.cnt[i]);
-#pragma unroll
-    for (int c = 0; c < NI; ++c) {
-      const unsigned long long v = sm.isum[(size_t)c * Lcap * kM + i];
-      if (v) atomicAdd(&p.prov_isum[c][g], v);
-    }
-#pragma unroll
-    for (int c = 0; c < NF; ++c) {
-      const double v = sm.fsum[(size_t)c * Lcap * kM + i];
-      if (v != 0.0) atomicAdd(&p.prov_fsum[c][g], v);
-    }
-    if (MM & 1) atomicMin(&p.prov_min[g], sm.emin[i]);
-    if (MM & 2) atomicMax(&p.prov_max[g], sm.emax[i]);
-  }
-  for (int s = tid; s < nloc; s += nth)
-    if (sm.lprov[s] >= 0 && sm.lrows[s]) atomicAdd(&p.prov_rows[sm.lprov[s]], sm.lrows[s]);
-  if (NI > 0) {
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      const unsigned long long o = __shfl_xor_sync(0xffffffffu, maxabs, d);
-      maxabs = o > maxabs ? o : maxabs;
-    }
-    if (lane == 0 && maxabs) atomicMax(p.gmaxabs, maxabs);
-  }
 }
 
 // ------------------------------------------------------------------ k_agg_minmax (pruned)
@@ -1335,7 +483,7 @@ static SmemLayout make_layout(const AccSet& A, int T, int Lcap, int key_bytes = 
   L.o_ival = take(A.ni * TS * 8);
   L.o_fval = take(A.nf * TS * 8);
   L.o_mval = take(mm ? TS * 8 : 0);
-  L.o_i32 = take(A.ni * TS * 4);
+  L.o_i32 = take(0);
   L.o_cnt = take(Lcap * kM * 4);
   L.o_lstate = take(L.LH * 4);
   L.o_lprov = take(Lcap * 4);
@@ -1360,8 +508,8 @@ static SmemLayout make_layout(const AccSet& A, int T, int Lcap, int key_bytes = 
 static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, int key_bytes, SmemLayout* out) {
   const int want = (int)std::min<int64_t>(std::max<int64_t>(G_cap, 1), 256);
   const char* force = getenv("PAC_TILE");
-  const int tiles_fixed[2] = {force ? atoi(force) : 1024, force ? atoi(force) : 512};
-  for (int per_sm : {3, 2}) {
+  const int tiles_fixed[2] = {force ? atoi(force) : 1024, force ? atoi(force) : 512};  // multiples of 512
+  for (int per_sm : {PAC_TILE_MINB, 3, 2}) {
     const int budget = smem_max / per_sm - 2048;
     for (int T : tiles_fixed) {
       SmemLayout L = make_layout(A, T, want, key_bytes);
@@ -1415,20 +563,43 @@ static MMLayout mm_layout(int64_t G_cap, int smem_max) {
   return L;
 }
 
-template <int NI, int NF, int MM>
-static cudaError_t launch_smem(const AggPlan& p, const SmemLayout& L, int sms, cudaStream_t st) {
-  auto k = k_agg_tiles<NI, NF, MM>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
-  if (e != cudaSuccess) return e;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTileThreads, L.bytes);
-  per_sm = std::max(1, per_sm);
-  const int64_t tiles = (p.n_rows + L.T - 1) / L.T;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * per_sm));
-  k<<<grid, kTileThreads, L.bytes, st>>>(p, L);
-  note_launch();
-  return cudaGetLastError();
-}
+// instantiated in agg_inst_ni{0,1,2}.cu
+extern template cudaError_t launch_smem<0, 0, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 0, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 0, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 0, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 1, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 1, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 1, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 1, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 2, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 2, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 2, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<0, 2, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 0, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 0, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 0, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 0, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 1, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 1, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 1, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 1, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 2, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 2, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 2, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<1, 2, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 0, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 0, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 0, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 0, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 1, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 1, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 1, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 1, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 2, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 2, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 2, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_smem<2, 2, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
 
 typedef cudaError_t (*LaunchFn)(const AggPlan&, const SmemLayout&, int, cudaStream_t);
 

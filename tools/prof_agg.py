@@ -27,7 +27,7 @@ def main():
     cols = dg.device_columns(w, 0, w.n_rows)
     kinds = [k for k, _ in w.aggs]
     vals = [None if i < 0 else cols["values"][i] for _, i in w.aggs]
-    G_cap = a.gcap or (64 if w.name in ("C1", "C2") else (4096 if w.name in ("C4", "C5") else 1 << 21))
+    G_cap = a.gcap or {"C1": 1, "C2": 8, "C4": 1024, "C5": 100}.get(w.name, 1 << 21)
     s = pac.Session(7, w.budget)
     ag = pac.Aggregator(kinds, G_cap)
     fin = pac.Finalizer(kinds, G_cap)
