@@ -629,8 +629,8 @@ __device__ __forceinline__ void tile_front(const AggPlan& p, const TileSmem& sm,
   // straight to the slot-sorted position; rows still needing flips are queued for A3.
   bool big = false, nonfin = false;
   for (int la = tid; la < T; la += 2 * nth) {
-    const int lb = la + nth;  // T is a multiple of 2 * nth
-    const unsigned short sa = sm.sslot[la], sb = sm.sslot[lb];
+    const int lb = la + nth;  // T is a multiple of nth; lb >= T when T < 2 * nth
+    const unsigned short sa = sm.sslot[la], sb = lb < T ? sm.sslot[lb] : kNone;
     const int pa = sa != kNone ? sm.ucnt[(la >> 5) * Lcap + sa] + sm.srank[la] : 0;
     const int pb = sb != kNone ? sm.ucnt[(lb >> 5) * Lcap + sb] + sm.srank[lb] : 0;
     bool qa = false, qb = false;
