@@ -11,6 +11,9 @@ namespace pac {
 
 constexpr int kThreads = 512;      // k_agg_minmax
 constexpr int kTileThreads = 256;  // k_agg_tiles
+#ifndef PAC_TILE_FLUSH
+#define PAC_TILE_FLUSH 0  // 1: warp accumulators flushed at the end of every tile's phase C
+#endif
 #ifndef PAC_TILE_MINB
 #define PAC_TILE_MINB 3  // min resident CTAs per SM the register allocation targets
 #endif
@@ -57,8 +60,8 @@ struct AggPlan {
 struct SmemLayout {
   int T, TS, Lcap, LH;
   int o_lkey, o_lstate, o_lprov, o_lrows, o_cnt, o_isum, o_fsum, o_min, o_max;
-  int o_mask, o_slot, o_rank, o_ucnt, o_queue, o_ival, o_i32, o_fval, o_mval, o_hist, o_offs,
-      o_runoffs, o_tcs, o_raw, o_mbar, o_misc;
+  int o_mask, o_slot, o_rank, o_ucnt, o_queue, o_ival, o_rdesc, o_fval, o_mval, o_hist, o_offs,
+      o_runoffs, o_xcs, o_raw, o_mbar, o_misc;
   int bytes;
 };
 
@@ -222,44 +225,89 @@ __device__ __forceinline__ void issue_tile(const AggPlan& p, unsigned char* raw,
     bulk_g2s(raw + p.raw_off[i], (const char*)p.raw_src[i] + base * p.raw_eb[i], (uint32_t)(T * p.raw_eb[i]), mbar);
 }
 
-// ------------------------------------------------------------------ k_agg_tiles (v3)
+// ------------------------------------------------------------------ k_agg_tiles (v4)
 // Bit-matrix transpose of a 32-row run: on input lane r holds row r's
 // 32-bit mask word; on output lane c holds the pattern of world c over the run.  Stage s
 // swaps the off-diagonal s x s blocks: the partner's word is rotated by s (low lane) or
 // 32-s (high lane) with one funnel shift and merged with one LOP3 under a per-lane mask.
-// Per-lane constants of the 5 stages live in shared memory (tcs[stage*32 + lane] =
-// {keep mask, rotate amount}), loaded once per run: cheaper than rematerialising them.
-__device__ __forceinline__ uint2 transpose_const(int lane, int i) {
-  const int s = 16 >> i;
-  const uint32_t M = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
-                   : s == 2 ? 0x33333333u : 0x55555555u;
-  const bool up = (lane & s) != 0;
-  return make_uint2(up ? ~M : M, (uint32_t)(up ? 32 - s : s));
-}
+// The per-lane constants live in registers: five keep masks and the five rotate amounts
+// packed 6 bits apart (the funnel shift only reads the low 5 bits of its amount).
+struct XposeConst {
+  uint32_t keep[5];
+  uint32_t amt;
+};
 
-__device__ __forceinline__ void transpose2x32(uint32_t& a, uint32_t& b, const uint2* __restrict__ tcs,
-                                              int lane) {
-  uint2 c[5];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) c[i] = tcs[i * 32 + lane];
+__device__ __forceinline__ XposeConst make_xpose(int lane) {
+  XposeConst c;
+  c.amt = 0;
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
     const int s = 16 >> i;
+    const uint32_t M = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
+                     : s == 2 ? 0x33333333u : 0x55555555u;
+    const bool up = (lane & s) != 0;
+    c.keep[i] = up ? ~M : M;
+    c.amt |= (uint32_t)(up ? 32 - s : s) << (6 * i);
+  }
+  return c;
+}
+
+// The constants of one lane, kept in shared memory (xcs[lane] = keep 0-3, xcs2[lane] = keep 4 and
+// the packed amounts) and loaded with two vector loads per run: cheaper than keeping six
+// registers live across the whole tile loop.
+__device__ __forceinline__ void store_xpose(uint4* xcs, uint2* xcs2, int lane) {
+  const XposeConst c = make_xpose(lane);
+  xcs[lane] = make_uint4(c.keep[0], c.keep[1], c.keep[2], c.keep[3]);
+  xcs2[lane] = make_uint2(c.keep[4], c.amt);
+}
+__device__ __forceinline__ XposeConst load_xpose(const uint4* xcs, const uint2* xcs2, int lane) {
+  XposeConst c;
+  const uint4 a = xcs[lane];
+  const uint2 b = xcs2[lane];
+  c.keep[0] = a.x;
+  c.keep[1] = a.y;
+  c.keep[2] = a.z;
+  c.keep[3] = a.w;
+  c.keep[4] = b.x;
+  c.amt = b.y;
+  return c;
+}
+
+__device__ __forceinline__ void transpose2x32(uint32_t& a, uint32_t& b, const XposeConst& c) {
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int s = 16 >> i;
+    const uint32_t r = c.amt >> (6 * i);
     const uint32_t ya = __shfl_xor_sync(0xffffffffu, a, s);
     const uint32_t yb = __shfl_xor_sync(0xffffffffu, b, s);
-    a = (a & c[i].x) | (__funnelshift_l(ya, ya, c[i].y) & ~c[i].x);
-    b = (b & c[i].x) | (__funnelshift_l(yb, yb, c[i].y) & ~c[i].x);
+    a = (a & c.keep[i]) | (__funnelshift_l(ya, ya, r) & ~c.keep[i]);
+    b = (b & c.keep[i]) | (__funnelshift_l(yb, yb, r) & ~c.keep[i]);
   }
 }
 
 __device__ __forceinline__ double shfl_d(double v, int src) {
-  const int lo = __shfl_sync(0xffffffffu, __double2loint(v), src);
-  const int hi = __shfl_sync(0xffffffffu, __double2hiint(v), src);
-  return __hiloint2double(hi, lo);
+  double r;
+  asm volatile(
+      "{\n .reg .b32 lo, hi, rlo, rhi;\n mov.b64 {lo, hi}, %1;\n"
+      " shfl.sync.idx.b32 rlo, lo, %2, 0x1f, 0xffffffff;\n"
+      " shfl.sync.idx.b32 rhi, hi, %2, 0x1f, 0xffffffff;\n mov.b64 %0, {rlo, rhi};\n}"
+      : "=d"(r) : "d"(v), "r"(src));
+  return r;
 }
 
 __device__ __forceinline__ bool finite_bits(double v) {
   return (__double2hiint(v) & 0x7FF00000) != 0x7FF00000;
+}
+
+// 64-bit add into shared memory as two 32-bit atomics (the carry of the low word is the
+// carry of this addition, whatever other adds interleave): cheaper than the CAS loop a
+// 64-bit shared-memory atomicAdd compiles to.
+__device__ __forceinline__ void smem_add_u64(unsigned long long* addr, unsigned long long v) {
+  unsigned* w = reinterpret_cast<unsigned*>(addr);
+  const unsigned lo = (unsigned)v, hi = (unsigned)(v >> 32);
+  const unsigned old = atomicAdd(w, lo);
+  const unsigned carry = (old + lo) < old ? 1u : 0u;
+  if (hi + carry) atomicAdd(w + 1, hi + carry);
 }
 
 // Register accumulators of the slot a warp is currently working on (lane: worlds lane, lane+32).
@@ -289,13 +337,13 @@ struct WarpAcc {
     if (c1) atomicAdd(&cnt[b + lane + 32], c1);
 #pragma unroll
     for (int c = 0; c < NI; ++c) {
-      atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane], (unsigned long long)ia0[c]);
-      atomicAdd(&isum[(size_t)c * Lcap * kM + b + lane + 32], (unsigned long long)ia1[c]);
+      smem_add_u64(&isum[(size_t)c * Lcap * kM + b + lane], (unsigned long long)ia0[c]);
+      smem_add_u64(&isum[(size_t)c * Lcap * kM + b + lane + 32], (unsigned long long)ia1[c]);
     }
 #pragma unroll
     for (int c = 0; c < NF; ++c) {
-      atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane], fa0[c]);
-      atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane + 32], fa1[c]);
+      if (fa0[c] != 0.0) atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane], fa0[c]);
+      if (fa1[c] != 0.0) atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane + 32], fa1[c]);
     }
     if (MM & 1) {
       atomicMin(&emin[b + lane], enc_f64(mn0));
@@ -309,144 +357,142 @@ struct WarpAcc {
   }
 };
 
+// Run descriptor (phase B): one 32-row run of one slot, packed into 32 bits.
+__device__ __forceinline__ uint32_t pack_run(int beg, int slot, int len) {
+  return (uint32_t)beg | ((uint32_t)slot << 16) | ((uint32_t)(len - 1) << 26);
+}
+
 struct RunCtx {  // read-only per-tile state of phase C
   const unsigned long long* smask;
   const long long* sival;
-  const int* si32;
   const double* sfval;
   const double* smval;
-  const int* hist;
-  const int* offs;
-  const int* runoffs;
-  const uint2* tcs;
+  const uint32_t* rdesc;
+  const uint4* xcs;
+  const uint2* xcs2;
   int TS, Lcap, R;
 };
 
-// Phase C of one tile for one warp: runs [r0, r1) of the tile's slot-sorted rows.
-// SMALL: int64 values of the tile fit int32 nibble tables; FIN: f64 values are finite, so
-// the f64 nibble tables are built with exact 0/1 FMAs.
-template <int NI, int NF, int MM, bool SMALL, bool FIN>
-__device__ __forceinline__ void run_tiles(WarpAcc<NI, NF, MM>& acc, const RunCtx& x, unsigned* cnt,
-                                          unsigned long long* isum, double* fsum, long long* emin,
-                                          long long* emax, int wid, int nw, int lane) {
-  const int R = x.R, TS = x.TS;
-  const int r0 = (int)(((long long)R * wid) / nw);
-  const int r1 = (int)(((long long)R * (wid + 1)) / nw);
-  if (r0 >= r1) return;
-  const int sub = lane & 15;
+// World-parallel update of one run of len <= 32 same-slot rows (row 0 at smask[0]; column c
+// of the int64 / f64 values at sival[c * istride] / sfval[c * fstride]).  Rows [len, 8*ceil(len/8))
+// must hold finite values (zero padding): they enter table entries that are never looked up.
+// SMALL: |int64 values| < 2^26, so 4-row subset sums and 32-row partials fit int32; FIN: the
+// f64 values are finite, so the f64 nibble tables are built with exact 0/1 FMAs.  Both hold
+// for the synthetic workloads; GENERIC instances test them at run time.
+template <int NI, int NF, int MM, bool GENERIC>
+__device__ __forceinline__ void run_body(WarpAcc<NI, NF, MM>& acc, const unsigned long long* __restrict__ smask,
+                                         const long long* __restrict__ sival, int istride,
+                                         const double* __restrict__ sfval, int fstride,
+                                         const double* __restrict__ smval, int len, const XposeConst& xc, int lane,
+                                         bool small_rt = true, bool fin_rt = true) {
+  // GENERIC = false: the common case (SMALL and FIN) with no runtime tests inside the loop
+  const bool SMALL = GENERIC ? small_rt : true;
+  const bool FIN = GENERIC ? fin_rt : true;
   const int tsrc = (lane >> 4) << 2;
-  const int ib0 = sub & 1, ib1 = (sub >> 1) & 1, ib2 = (sub >> 2) & 1, ib3 = (sub >> 3) & 1;
+  const int ib0 = lane & 1, ib1 = (lane >> 1) & 1, ib2 = (lane >> 2) & 1, ib3 = (lane >> 3) & 1;
   const double db0 = ib0, db1 = ib1, db2 = ib2, db3 = ib3;
-  int s;
-  {
-    int lo = 0, hi = x.Lcap;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (x.runoffs[mid] <= r0) lo = mid; else hi = mid - 1;
+  const uint64_t m = lane < len ? smask[lane] : 0ull;
+  uint32_t P = (uint32_t)m, Q = (uint32_t)(m >> 32);
+  transpose2x32(P, Q, xc);
+  acc.c0 += __popc(P);
+  acc.c1 += __popc(Q);
+  // nibble indices: table A (lanes 0-15) covers rows 8q..8q+3, B (16-31) rows 8q+4..8q+7;
+  // shfl uses only the low 5 bits of the source lane.
+  const uint32_t PA = P & 0x0F0F0F0Fu, PB = ((P >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
+  const uint32_t QA = Q & 0x0F0F0F0Fu, QB = ((Q >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
+  const int nq = (len + 7) >> 3;
+  int rs0[NI > 0 ? NI : 1], rs1[NI > 0 ? NI : 1];
+#pragma unroll
+  for (int c = 0; c < NI; ++c) rs0[c] = rs1[c] = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q >= nq) break;
+    const int a0 = (int)(PA >> (8 * q)), b0 = (int)(PB >> (8 * q));
+    const int a1 = (int)(QA >> (8 * q)), b1 = (int)(QB >> (8 * q));
+    const int row = 8 * q + tsrc;
+#pragma unroll
+    for (int c = 0; c < NI; ++c) {
+      const longlong2 u = *(const longlong2*)(sival + c * istride + row);
+      const longlong2 w = *(const longlong2*)(sival + c * istride + row + 2);
+      if (SMALL) {
+        const int t = (int)u.x * ib0 + (int)u.y * ib1 + (int)w.x * ib2 + (int)w.y * ib3;
+        rs0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
+        rs1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
+      } else {
+        const long long t = u.x * ib0 + u.y * ib1 + w.x * ib2 + w.y * ib3;
+        acc.ia0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
+        acc.ia1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
+      }
     }
-    s = lo;
+#pragma unroll
+    for (int c = 0; c < NF; ++c) {
+      const double2 u = *(const double2*)(sfval + c * fstride + row);
+      const double2 w = *(const double2*)(sfval + c * fstride + row + 2);
+      double t;
+      if (FIN) {  // exact: 0*v + t == t and 1*v + t == v + t for finite v
+        t = fma(db3, w.y, fma(db2, w.x, fma(db1, u.y, db0 * u.x)));
+      } else {
+        t = ib0 ? u.x : 0.0;
+        if (ib1) t += u.y;
+        if (ib2) t += w.x;
+        if (ib3) t += w.y;
+      }
+      acc.fa0[c] += shfl_d(t, a0);
+      acc.fa0[c] += shfl_d(t, b0);
+      acc.fa1[c] += shfl_d(t, a1);
+      acc.fa1[c] += shfl_d(t, b1);
+    }
+    if (MM) {
+      const double2 u = *(const double2*)(smval + row);
+      const double2 w = *(const double2*)(smval + row + 2);
+      if (MM & 1) {
+        double t = ib0 ? u.x : INFINITY;
+        if (ib1) t = fmin(t, u.y);
+        if (ib2) t = fmin(t, w.x);
+        if (ib3) t = fmin(t, w.y);
+        acc.mn0 = fmin(acc.mn0, fmin(shfl_d(t, a0), shfl_d(t, b0)));
+        acc.mn1 = fmin(acc.mn1, fmin(shfl_d(t, a1), shfl_d(t, b1)));
+      }
+      if (MM & 2) {
+        double t = ib0 ? u.x : -INFINITY;
+        if (ib1) t = fmax(t, u.y);
+        if (ib2) t = fmax(t, w.x);
+        if (ib3) t = fmax(t, w.y);
+        acc.mx0 = fmax(acc.mx0, fmax(shfl_d(t, a0), shfl_d(t, b0)));
+        acc.mx1 = fmax(acc.mx1, fmax(shfl_d(t, a1), shfl_d(t, b1)));
+      }
+    }
   }
-  int rs_end = x.runoffs[s + 1];
-  int k0 = 32 * (r0 - x.runoffs[s]);
-  int slot_beg = x.offs[s], slot_len = x.hist[s];
-  for (int r = r0; r < r1; ++r) {
-    if (r >= rs_end) {  // next non-empty slot
-      do {
-        ++s;
-        rs_end = x.runoffs[s + 1];
-      } while (rs_end <= r);
-      k0 = 0;
-      slot_beg = x.offs[s];
-      slot_len = x.hist[s];
+  if (SMALL) {
+#pragma unroll
+    for (int c = 0; c < NI; ++c) {
+      acc.ia0[c] += rs0[c];
+      acc.ia1[c] += rs1[c];
     }
+  }
+}
+
+// Phase C of one tile for one warp: runs [r0, r1) of the tile's slot-sorted rows.
+template <int NI, int NF, int MM, bool GENERIC>
+__device__ __forceinline__ void run_tiles(WarpAcc<NI, NF, MM>& acc, const RunCtx& x,
+                                          unsigned* cnt, unsigned long long* isum, double* fsum, long long* emin,
+                                          long long* emax, int wid, int nw, int lane, bool small, bool fin) {
+  const int R = x.R, TS = x.TS;
+  const int r0 = (R * wid) / nw;
+  const int r1 = (R * (wid + 1)) / nw;
+#pragma unroll 1
+  for (int r = r0; r < r1; ++r) {
+    const uint32_t d = x.rdesc[r];
+    const int beg = (int)(d & 0xFFFFu);
+    const int s = (int)((d >> 16) & 0x3FFu);
+    const int len = (int)(d >> 26) + 1;
     if (s != acc.cur) {
       acc.flush(cnt, isum, fsum, emin, emax, x.Lcap, lane);
       acc.cur = s;
     }
-    const int beg = slot_beg + k0;
-    const int len = min(32, slot_len - k0);
-    k0 += 32;
-    const uint64_t m = lane < len ? x.smask[beg + lane] : 0ull;
-    uint32_t P = (uint32_t)m, Q = (uint32_t)(m >> 32);
-    transpose2x32(P, Q, x.tcs, lane);
-    acc.c0 += __popc(P);
-    acc.c1 += __popc(Q);
-    // nibble indices: table A (lanes 0-15) covers rows 8q..8q+3, B (16-31) rows 8q+4..8q+7;
-    // shfl uses only the low 5 bits of the source lane.
-    const uint32_t PA = P & 0x0F0F0F0Fu, PB = ((P >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
-    const uint32_t QA = Q & 0x0F0F0F0Fu, QB = ((Q >> 4) & 0x0F0F0F0Fu) | 0x10101010u;
-    const int nq = (len + 7) >> 3;
-    int rs0[NI > 0 ? NI : 1], rs1[NI > 0 ? NI : 1];
-#pragma unroll
-    for (int c = 0; c < NI; ++c) rs0[c] = rs1[c] = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (q >= nq) break;
-      const int a0 = (int)(PA >> (8 * q)), b0 = (int)(PB >> (8 * q));
-      const int a1 = (int)(QA >> (8 * q)), b1 = (int)(QB >> (8 * q));
-      const int row = beg + 8 * q + tsrc;
-#pragma unroll
-      for (int c = 0; c < NI; ++c) {
-        if (SMALL) {
-          const longlong2 u = *(const longlong2*)(x.sival + c * TS + row);
-          const longlong2 w = *(const longlong2*)(x.sival + c * TS + row + 2);
-          const int t = (int)u.x * ib0 + (int)u.y * ib1 + (int)w.x * ib2 + (int)w.y * ib3;
-          rs0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
-          rs1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
-        } else {
-          const longlong2 u = *(const longlong2*)(x.sival + c * TS + row);
-          const longlong2 w = *(const longlong2*)(x.sival + c * TS + row + 2);
-          const long long t = u.x * ib0 + u.y * ib1 + w.x * ib2 + w.y * ib3;
-          acc.ia0[c] += __shfl_sync(0xffffffffu, t, a0) + __shfl_sync(0xffffffffu, t, b0);
-          acc.ia1[c] += __shfl_sync(0xffffffffu, t, a1) + __shfl_sync(0xffffffffu, t, b1);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < NF; ++c) {
-        const double2 u = *(const double2*)(x.sfval + c * TS + row);
-        const double2 w = *(const double2*)(x.sfval + c * TS + row + 2);
-        double t;
-        if (FIN) {  // exact: 0*v + t == t and 1*v + t == v + t for finite v
-          t = fma(db3, w.y, fma(db2, w.x, fma(db1, u.y, db0 * u.x)));
-        } else {
-          t = ib0 ? u.x : 0.0;
-          if (ib1) t += u.y;
-          if (ib2) t += w.x;
-          if (ib3) t += w.y;
-        }
-        acc.fa0[c] += shfl_d(t, a0);
-        acc.fa0[c] += shfl_d(t, b0);
-        acc.fa1[c] += shfl_d(t, a1);
-        acc.fa1[c] += shfl_d(t, b1);
-      }
-      if (MM) {
-        const double2 u = *(const double2*)(x.smval + row);
-        const double2 w = *(const double2*)(x.smval + row + 2);
-        if (MM & 1) {
-          double t = ib0 ? u.x : INFINITY;
-          if (ib1) t = fmin(t, u.y);
-          if (ib2) t = fmin(t, w.x);
-          if (ib3) t = fmin(t, w.y);
-          acc.mn0 = fmin(acc.mn0, fmin(shfl_d(t, a0), shfl_d(t, b0)));
-          acc.mn1 = fmin(acc.mn1, fmin(shfl_d(t, a1), shfl_d(t, b1)));
-        }
-        if (MM & 2) {
-          double t = ib0 ? u.x : -INFINITY;
-          if (ib1) t = fmax(t, u.y);
-          if (ib2) t = fmax(t, w.x);
-          if (ib3) t = fmax(t, w.y);
-          acc.mx0 = fmax(acc.mx0, fmax(shfl_d(t, a0), shfl_d(t, b0)));
-          acc.mx1 = fmax(acc.mx1, fmax(shfl_d(t, a1), shfl_d(t, b1)));
-        }
-      }
-    }
-    if (SMALL) {
-#pragma unroll
-      for (int c = 0; c < NI; ++c) {
-        acc.ia0[c] += rs0[c];
-        acc.ia1[c] += rs1[c];
-      }
-    }
+    const XposeConst xc = load_xpose(x.xcs, x.xcs2, lane);
+    run_body<NI, NF, MM, GENERIC>(acc, x.smask + beg, x.sival + beg, TS, x.sfval + beg, TS, x.smval + beg, len,
+                                  xc, lane, small, fin);
   }
 }
 
@@ -462,7 +508,7 @@ struct TileSmem {
   long long* emax;
   unsigned long long* smask;  // [TS] slot-sorted masks
   long long* sival;           // [NI][TS]
-  int* si32;                  // [NI][TS]
+  uint32_t* rdesc;            // [runs] run descriptors (pack_run)
   double* sfval;              // [NF][TS]
   double* smval;              // [TS]
   unsigned short* sslot;      // [T]
@@ -473,9 +519,10 @@ struct TileSmem {
   int* hist;
   int* offs;
   int* runoffs;
-  uint2* tcs;
+  uint4* xcs;                 // [32] transpose constants (store_xpose)
+  uint2* xcs2;                // [32]
   Misc* misc;
-  const unsigned char* raw;   // staged raw tile: 8-byte columns k at k*T*8, then key columns
+  unsigned char* raw;         // staged raw tile: 8-byte columns k at k*T*8, then key columns
 };
 
 // Column k of the tile: 0 = pu_key/mask, 1..NI int64 sums, NI+1..NI+NF f64 sums, then the
@@ -514,24 +561,24 @@ struct TileCols {
   }
 };
 
-// A1 (slots + ranks), B (offsets), A2 (hash word 0 + sorted staging), A3 (stragglers) of one
-// tile.  Leaves the slot-sorted tile in smem and the run table for phase C.
+// Per-tile phases.  Pipeline of one CTA, 4 barriers per tile:
+//   [C(t-1) | A1(t)]  sync  B2(t)  sync  B3(t)  sync  A2+A3(t)  sync  -> [C(t) | A1(t+1)] ...
+// A1 touches only sslot/srank/ucnt/hist and the dictionary, C only the slot-sorted staging
+// and the run table, so a warp runs its share of C(t) and then its share of A1(t+1) with no
+// barrier in between.
+
+// A1: group slot of every row, rank within its 32-row unit, per-unit and per-tile slot counts.
 template <int NI, int NF, int MM, bool STAGED>
-__device__ __forceinline__ void tile_front(const AggPlan& p, const TileSmem& sm, const SmemLayout& L, int64_t base,
-                                           int tn, unsigned long long& maxabs) {
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int lane = tid & 31, wid = tid >> 5;
-  const int T = L.T, TS = L.TS, Lcap = L.Lcap, LH = L.LH;
-  const int units = T >> 5;
+__device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, const SmemLayout& L, int64_t base,
+                                        int tn) {
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31;
+  const int T = L.T, Lcap = L.Lcap, LH = L.LH;
   const unsigned short kNone = 0xFFFF;
   const unsigned lt_mask = (1u << lane) - 1u;
-  constexpr int KF = 1 + NI;             // first f64 sum column
-  constexpr int KM = 1 + NI + NF;        // min/max column
-  constexpr int KK = 1 + NI + NF + (MM ? 1 : 0);  // first group-key column
+  constexpr int KF = 1 + NI;
+  constexpr int KM = 1 + NI + NF;
+  constexpr int KK = 1 + NI + NF + (MM ? 1 : 0);
   TileCols<STAGED> tc{&p, sm.raw, base, T};
-  Misc* misc = sm.misc;
-
-  // ---------------- A1: group slot of every row + rank within its 32-row unit
   for (int li = tid; li < T; li += nth) {
     int s = -1;
     if (li < tn) {
@@ -539,7 +586,7 @@ __device__ __forceinline__ void tile_front(const AggPlan& p, const TileSmem& sm,
       if (p.mask_in) keep = tc.w8(0, li) != 0ull;  // R21: a row in no world is dropped
       if (keep) {
         const uint64_t key = tc.group_key(KK, li);
-        const int code = local_code(p, key, sm.lkey, sm.lstate, LH, sm.lprov, Lcap, misc);
+        const int code = local_code(p, key, sm.lkey, sm.lstate, LH, sm.lprov, Lcap, sm.misc);
         if (code < kOvfBase) {
           s = code - 1;
         } else {  // no local slot: straight to the HBM table (rare)
@@ -556,21 +603,41 @@ __device__ __forceinline__ void tile_front(const AggPlan& p, const TileSmem& sm,
       }
     }
     const unsigned peers = __match_any_sync(0xffffffffu, s >= 0 ? (unsigned)s : 0x10000u + lane);
+    unsigned short* uc = sm.ucnt + (li >> 5) * Lcap;
+    if (Lcap <= 32) {  // this unit's counts start at zero
+      if (lane < Lcap) uc[lane] = 0;
+    } else {
+      for (int z = lane; z < Lcap; z += 32) uc[z] = 0;
+    }
+    __syncwarp();
     if (s >= 0) {
       sm.srank[li] = (unsigned char)__popc(peers & lt_mask);
-      if ((peers & lt_mask) == 0) sm.ucnt[(li >> 5) * Lcap + s] = (unsigned short)__popc(peers);
+      if ((peers & lt_mask) == 0) {
+        uc[s] = (unsigned short)__popc(peers);
+        atomicAdd(&sm.hist[s], __popc(peers));
+      }
     }
     sm.sslot[li] = s >= 0 ? (unsigned short)s : kNone;
   }
-  __syncthreads();
+}
 
-  // ---------------- B: slot totals, 8-row padded offsets, run offsets, unit positions
-  for (int s = tid; s < Lcap; s += nth) {
-    int tot = 0;
-    for (int u = 0; u < units; ++u) tot += sm.ucnt[u * Lcap + s];
-    sm.hist[s] = tot;
-  }
-  __syncthreads();
+// B2 + B3 + A2 + A3 of one tile (A1 done, hist complete).  Leaves the slot-sorted tile in smem
+// and the run table for phase C; ends with a barrier.
+template <int NI, int NF, int MM, bool STAGED>
+__device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, const SmemLayout& L, int64_t base,
+                                         unsigned long long& maxabs) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  const int T = L.T, TS = L.TS, Lcap = L.Lcap;
+  const int units = T >> 5;
+  const unsigned short kNone = 0xFFFF;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  constexpr int KF = 1 + NI;             // first f64 sum column
+  constexpr int KM = 1 + NI + NF;        // min/max column
+  TileCols<STAGED> tc{&p, sm.raw, base, T};
+  Misc* misc = sm.misc;
+
+  // ---------------- B2: 8-row padded slot offsets and run offsets (one warp)
   if (wid == 0) {
     const int per = (Lcap + 31) / 32;
     const int s0 = lane * per;
@@ -601,9 +668,12 @@ __device__ __forceinline__ void tile_front(const AggPlan& p, const TileSmem& sm,
     if (lane == 31) {
       sm.runoffs[Lcap] = rx;
       misc->nruns = rx;
+      misc->big = 0;
+      misc->nonfinite = 0;
     }
   }
   __syncthreads();
+  // ---------------- B3: unit positions, zero padding rows, run descriptors
   for (int s = tid; s < Lcap; s += nth) {
     const int o0 = sm.offs[s];
     int o = o0;
@@ -612,22 +682,27 @@ __device__ __forceinline__ void tile_front(const AggPlan& p, const TileSmem& sm,
       sm.ucnt[u * Lcap + s] = (unsigned short)o;
       o += c;
     }
-    for (int q = o; q < o0 + ((sm.hist[s] + 7) & ~7); ++q) {  // zero padding rows (mask 0)
+    const int h = sm.hist[s];
+    for (int q = o; q < o0 + ((h + 7) & ~7); ++q) {  // zero padding rows (mask 0)
       sm.smask[q] = 0;
 #pragma unroll
-      for (int c = 0; c < NI; ++c) {
-        sm.sival[c * TS + q] = 0;
-      }
+      for (int c = 0; c < NI; ++c) sm.sival[c * TS + q] = 0;
 #pragma unroll
       for (int c = 0; c < NF; ++c) sm.sfval[c * TS + q] = 0.0;
       if (MM) sm.smval[q] = 0.0;
     }
+    for (int i = 0, rb = sm.runoffs[s]; 32 * i < h; ++i)
+      sm.rdesc[rb + i] = pack_run(o0 + 32 * i, s, min(32, h - 32 * i));
+    sm.hist[s] = 0;  // ready for the next tile's A1
   }
   __syncthreads();
 
   // ---------------- A2: hash word 0 (two rows per thread, interleaved) + values, written
-  // straight to the slot-sorted position; rows still needing flips are queued for A3.
+  // straight to the slot-sorted position; rows still needing flips go to the warp's queue.
   bool big = false, nonfin = false;
+  unsigned short* qpos = sm.qpos + wid * (T / nw);
+  unsigned short* qrow = sm.qrow + wid * (T / nw);
+  int qn = 0;
   for (int la = tid; la < T; la += 2 * nth) {
     const int lb = la + nth;  // T is a multiple of nth; lb >= T when T < 2 * nth
     const unsigned short sa = sm.sslot[la], sb = lb < T ? sm.sslot[lb] : kNone;
@@ -644,10 +719,13 @@ __device__ __forceinline__ void tile_front(const AggPlan& p, const TileSmem& sm,
       } else {
         pac_hash_begin2(ka, kb, p.salt, ha, hb);
       }
-      ma = ha.x ^ (((__popcll(ha.x) > 32) ? ha.x : ~ha.x) ^ ha.cand);
-      mb = hb.x ^ (((__popcll(hb.x) > 32) ? hb.x : ~hb.x) ^ hb.cand);
+      ma = hash_mask_now(ha);
+      mb = hash_mask_now(hb);
       qa = sa != kNone && ha.k > 0;
       qb = sb != kNone && hb.k > 0;
+      // a queued row keeps its draw word 0 in the (consumed) key slot of the staged tile
+      if (STAGED && qa) ((unsigned long long*)sm.raw)[la] = ha.w0;
+      if (STAGED && qb) ((unsigned long long*)sm.raw)[lb] = hb.w0;
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -675,47 +753,27 @@ __device__ __forceinline__ void tile_front(const AggPlan& p, const TileSmem& sm,
     for (int h = 0; h < 2; ++h) {
       const bool pend = h ? qb : qa;
       const unsigned pm = __ballot_sync(0xffffffffu, pend);
-      int qbase = 0;
-      if (lane == 0 && pm) qbase = atomicAdd(&misc->nqueue, __popc(pm));
-      qbase = __shfl_sync(0xffffffffu, qbase, 0) + __popc(pm & lt_mask);
       if (pend) {
-        sm.qpos[qbase] = (unsigned short)(h ? pb : pa);
-        sm.qrow[qbase] = (unsigned short)(h ? lb : la);
+        const int q = qn + __popc(pm & lt_mask);
+        qpos[q] = (unsigned short)(h ? pb : pa);
+        qrow[q] = (unsigned short)(h ? lb : la);
       }
+      qn += __popc(pm);
     }
   }
   if (NI > 0 && __any_sync(0xffffffffu, big) && lane == 0) misc->big = 1;
   if (NF > 0 && __any_sync(0xffffffffu, nonfin) && lane == 0) misc->nonfinite = 1;
-  __syncthreads();
+  __syncwarp();
 
-  // ---------------- A3: finish the queued masks.  State re-derived from the key and the
-  // partial mask: cand = majority positions of the current word, k = |popcount - 32|.
-  // Every queued row draws word 1 branch-free; the ~5% of them still short (0.9% of all
-  // rows) finish in a per-row loop.
+  // ---------------- A3: the warp finishes its own queued masks from draw word 1 on (state
+  // re-derived from the partial mask, R2; word 0 from the staged key slot, or recomputed).
   if (!(p.ablate & 2)) {
-    const int qn = misc->nqueue;
-    for (int qi = tid; qi < qn; qi += nth) {
-      const int pos = sm.qpos[qi];
-      const uint64_t x = fmix64(tc.w8(0, sm.qrow[qi]) ^ p.salt);
-      const uint64_t m = sm.smask[pos];
-      const bool maj = __popcll(x) > 32;
-      uint64_t cand = maj ? m : ~m;
-      int k = abs(__popcll(m) - 32);
-      uint64_t w = fmix64(fmix64(x ^ kDrawSeed) + kDrawStep);  // word 1
-      draw_word(w, cand, k);
-      if (k > 0) {
-#pragma unroll 1
-        for (int word = 2; word < 64 && k > 0; ++word) {
-          w = fmix64(w + kDrawStep);
-          draw_word(w, cand, k);
-        }
-        while (k > 0) {  // safety net of R2
-          const uint64_t low = cand & (~cand + 1ull);
-          cand ^= low;
-          --k;
-        }
-      }
-      sm.smask[pos] = maj ? cand : ~cand;
+    for (int qi = lane; qi < qn; qi += 32) {
+      const int pos = qpos[qi];
+      const int li = qrow[qi];
+      const uint64_t w0 = STAGED ? ((const unsigned long long*)sm.raw)[li]
+                                 : fmix64(fmix64(tc.w8(0, li) ^ p.salt) ^ kDrawSeed);
+      sm.smask[pos] = pac_hash_continue(sm.smask[pos], w0);
     }
   }
   __syncthreads();
@@ -738,7 +796,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
   sm.emax = (long long*)(smem + L.o_max);
   sm.smask = (unsigned long long*)(smem + L.o_mask);
   sm.sival = (long long*)(smem + L.o_ival);
-  sm.si32 = (int*)(smem + L.o_i32);
+  sm.rdesc = (uint32_t*)(smem + L.o_rdesc);
   sm.sfval = (double*)(smem + L.o_fval);
   sm.smval = (double*)(smem + L.o_mval);
   sm.sslot = (unsigned short*)(smem + L.o_slot);
@@ -749,7 +807,8 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
   sm.hist = (int*)(smem + L.o_hist);
   sm.offs = (int*)(smem + L.o_offs);
   sm.runoffs = (int*)(smem + L.o_runoffs);
-  sm.tcs = (uint2*)(smem + L.o_tcs);
+  sm.xcs = (uint4*)(smem + L.o_xcs);
+  sm.xcs2 = (uint2*)(smem + L.o_xcs + 32 * 16);
   sm.misc = (Misc*)(smem + L.o_misc);
   unsigned char* raw = smem + L.o_raw;
   sm.raw = raw;
@@ -762,7 +821,10 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
   const int units = T >> 5;
 
   for (int i = tid; i < LH; i += nth) sm.lstate[i] = 0;
-  for (int i = tid; i < Lcap; i += nth) sm.lrows[i] = 0;
+  for (int i = tid; i < Lcap; i += nth) {
+    sm.lrows[i] = 0;
+    sm.hist[i] = 0;
+  }
   for (int i = tid; i < Lcap * kM; i += nth) {
     sm.cnt[i] = 0;
 #pragma unroll
@@ -772,14 +834,11 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
     if (MM & 1) sm.emin[i] = kEncPosInf;
     if (MM & 2) sm.emax[i] = kEncNegInf;
   }
-  if (tid < 32) {
-#pragma unroll
-    for (int i = 0; i < 5; ++i) sm.tcs[i * 32 + tid] = transpose_const(tid, i);
-  }
   if (tid == 0) {
     misc->nlocal = 0;
     misc->ndict = 0;
   }
+  if (tid < 32) store_xpose(sm.xcs, sm.xcs2, tid);
   unsigned long long maxabs = 0;
 
   const int64_t ntiles = (p.n_rows + T - 1) / T;
@@ -788,6 +847,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
   const int64_t t1 = min(ntiles, t0 + t_per);
   // a tile is staged by TMA when it is full and every column is 16-byte aligned
   auto staged_tile = [&](int64_t t) { return p.tma_ok && t < t1 && (t + 1) * T <= p.n_rows; };
+  auto tile_rows = [&](int64_t t) { return (int)min((int64_t)T, p.n_rows - t * T); };
   uint32_t phase = 0;
   if (tid == 0) {
     mbar_init(mbar, 1);
@@ -795,59 +855,76 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
   }
   __syncthreads();
 
+#if !PAC_TILE_FLUSH
   WarpAcc<NI, NF, MM> acc;
   acc.cur = -1;
   acc.reset();
+#endif
 
-  for (int64_t tile = t0; tile < t1; ++tile) {
-    const int64_t base = tile * T;
-    const int tn = (int)min((int64_t)T, p.n_rows - base);
-    for (int i = tid; i < units * Lcap; i += nth) sm.ucnt[i] = 0;
-    if (tid == 0) {
-      misc->big = 0;
-      misc->nonfinite = 0;
-      misc->nqueue = 0;
-    }
-    const bool staged = staged_tile(tile);
-    if (staged) {
+  // prologue: A1 of the first tile
+  if (t0 < t1) {
+    if (staged_tile(t0)) {
       mbar_wait(mbar, phase);
       phase ^= 1u;
+      tile_a1<NI, NF, MM, true>(p, sm, L, t0 * T, tile_rows(t0));
+    } else {
+      tile_a1<NI, NF, MM, false>(p, sm, L, t0 * T, tile_rows(t0));
     }
-    __syncthreads();
-    if (staged) tile_front<NI, NF, MM, true>(p, sm, L, base, tn, maxabs);
-    else tile_front<NI, NF, MM, false>(p, sm, L, base, tn, maxabs);
+  }
+  for (int64_t tile = t0; tile < t1; ++tile) {
+    const int64_t base = tile * T;
+    const bool staged = staged_tile(tile);
+    __syncthreads();  // A1(tile) and C(tile-1) complete
+    if (staged) tile_mid<NI, NF, MM, true>(p, sm, L, base, maxabs);
+    else tile_mid<NI, NF, MM, false>(p, sm, L, base, maxabs);
     // the raw tile buffer is free: stage the next tile while phase C runs
-    if (tid == 0 && staged_tile(tile + 1)) issue_tile(p, raw, mbar, (tile + 1) * T, T);
+    const bool next_staged = staged_tile(tile + 1);
+    if (tid == 0 && next_staged) issue_tile(p, raw, mbar, (tile + 1) * T, T);
 
     // ---------------- C: world-parallel runs, transposed "Four Russians" tables
     if (!(p.ablate & 4)) {
       RunCtx x;
       x.smask = sm.smask;
       x.sival = sm.sival;
-      x.si32 = sm.si32;
       x.sfval = sm.sfval;
       x.smval = sm.smval;
-      x.hist = sm.hist;
-      x.offs = sm.offs;
-      x.runoffs = sm.runoffs;
-      x.tcs = sm.tcs;
+      x.rdesc = sm.rdesc;
+      x.xcs = sm.xcs;
+      x.xcs2 = sm.xcs2;
       x.TS = L.TS;
       x.Lcap = Lcap;
       x.R = misc->nruns;
       const bool small = (NI == 0) || misc->big == 0;
       const bool fin = (NF == 0) || misc->nonfinite == 0;
+#if PAC_TILE_FLUSH
+      // accumulators live only inside phase C (not across the register-heavy front phases)
+      WarpAcc<NI, NF, MM> acc;
+      acc.cur = -1;
+      acc.reset();
+#endif
       if (small && fin)
-        run_tiles<NI, NF, MM, true, true>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
-      else if (small)
-        run_tiles<NI, NF, MM, true, false>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
-      else if (fin)
-        run_tiles<NI, NF, MM, false, true>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
+        run_tiles<NI, NF, MM, false>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane, true, true);
       else
-        run_tiles<NI, NF, MM, false, false>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane);
+        run_tiles<NI, NF, MM, true>(acc, x, sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, wid, nw, lane, small, fin);
+#if PAC_TILE_FLUSH
+      acc.flush(sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, Lcap, lane);
+#endif
     }
-    __syncthreads();
+    // ---------------- A1 of the next tile (disjoint smem; no barrier needed)
+    if (tile + 1 < t1) {
+      if (next_staged) {
+        mbar_wait(mbar, phase);
+        phase ^= 1u;
+        tile_a1<NI, NF, MM, true>(p, sm, L, base + T, tile_rows(tile + 1));
+      } else {
+        tile_a1<NI, NF, MM, false>(p, sm, L, base + T, tile_rows(tile + 1));
+      }
+    }
   }
+  __syncthreads();
+#if !PAC_TILE_FLUSH
   acc.flush(sm.cnt, sm.isum, sm.fsum, sm.emin, sm.emax, Lcap, lane);
+#endif
   __syncthreads();
 
   // ---------------- CTA table -> provisional HBM table

@@ -27,25 +27,31 @@ __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
 // pac_hash (§2, §4, R1 + R2 "rejection flips").
 // `cand` holds the positions that still carry the majority value; a draw that lands on one
 // flips it (k--).  The final mask is x ^ (cand_initial ^ cand_final).  Draws are processed
-// one 10-draw word at a time, branch-free inside the word (a lane with k == 0 keeps
-// drawing without effect), so a warp diverges only at word granularity.
+// one 10-draw word at a time, branch-free inside the word, so a warp diverges only at word
+// granularity.  One draw: the one-hot of its 6-bit position is gated by min(k, 1), so once
+// k == 0 the draw is a no-op; clearing the one-hot from `cand` flips the position exactly
+// when it still carries the majority value (~10 SASS per draw: SHF, LOP3, VIMNMX, 2 SHF for
+// the 64-bit one-hot, 3 LOP3 for the test and the clear, IADD/select for k).
 constexpr uint64_t kDrawSeed = 0xD1B54A32D192ED03ull;
 constexpr uint64_t kDrawStep = 0x9E3779B97F4A7C15ull;
 
+__device__ __forceinline__ void draw_step(uint64_t w, int t, uint64_t& cand, int& k) {
+  const uint32_t f = (uint32_t)(w >> (6 * t)) & 63u;
+  const uint64_t oh = (uint64_t)(uint32_t)min(k, 1) << f;
+  const bool hit = (cand & oh) != 0ull;
+  cand &= ~oh;
+  k -= hit ? 1 : 0;
+}
+
 __device__ __forceinline__ void draw_word(uint64_t w, uint64_t& cand, int& k) {
 #pragma unroll
-  for (int t = 0; t < 10; ++t) {
-    const uint32_t p = (uint32_t)(w >> (6 * t)) & 63u;
-    uint64_t hit = cand & (1ull << p);
-    hit = (k > 0) ? hit : 0ull;
-    cand ^= hit;
-    k -= (hit != 0ull) ? 1 : 0;
-  }
+  for (int t = 0; t < 10; ++t) draw_step(w, t, cand, k);
 }
 
 struct HashState {
   uint64_t x;     // fmix64(key ^ salt)
   uint64_t cand;  // current majority positions
+  uint64_t w0;    // draw word 0 = fmix64(x ^ kDrawSeed)
   int k;          // flips still needed
 };
 
@@ -56,15 +62,18 @@ __device__ __forceinline__ HashState pac_hash_begin(uint64_t key, uint64_t salt)
   const int c = __popcll(h.x);
   h.k = (c > 32) ? (c - 32) : (32 - c);
   h.cand = (c > 32) ? h.x : ~h.x;
-  if (h.k > 0) draw_word(fmix64(h.x ^ kDrawSeed), h.cand, h.k);
+  h.w0 = fmix64(h.x ^ kDrawSeed);
+  draw_word(h.w0, h.cand, h.k);
   return h;
 }
 
-// Continues from word 1 until k == 0 (or the R2 safety net).  `mask_now` is the mask
-// after word 0, i.e. x ^ (cand_initial ^ cand).
-__device__ __forceinline__ uint64_t pac_hash_finish(uint64_t x, uint64_t cand, int k) {
-  const uint64_t cand0 = (__popcll(x) > 32) ? x : ~x;
-  uint64_t w = fmix64(x ^ kDrawSeed);
+// Continues from the state after word `word0` (its draw word `w`) until k == 0 (or the R2
+// safety net); `m` is the mask after that word.  The majority value is recovered from `m`:
+// while k > 0 the mask still has popcount on the majority side.
+__device__ __forceinline__ uint64_t pac_hash_continue(uint64_t m, uint64_t w) {
+  const bool maj = __popcll(m) > 32;
+  uint64_t cand = maj ? m : ~m;
+  int k = maj ? (__popcll(m) - 32) : (32 - __popcll(m));
 #pragma unroll 1
   for (int word = 1; word < 64 && k > 0; ++word) {
     w = fmix64(w + kDrawStep);
@@ -75,18 +84,10 @@ __device__ __forceinline__ uint64_t pac_hash_finish(uint64_t x, uint64_t cand, i
     cand ^= low;
     --k;
   }
-  return x ^ (cand0 ^ cand);
+  return maj ? cand : ~cand;
 }
 
 // Two independent keys, their draws interleaved so the two dependency chains overlap.
-__device__ __forceinline__ void draw_step(uint64_t w, int t, uint64_t& cand, int& k) {
-  const uint32_t p = (uint32_t)(w >> (6 * t)) & 63u;
-  uint64_t hit = cand & (1ull << p);
-  hit = (k > 0) ? hit : 0ull;
-  cand ^= hit;
-  k -= (hit != 0ull) ? 1 : 0;
-}
-
 __device__ __forceinline__ void pac_hash_begin2(uint64_t ka, uint64_t kb, uint64_t salt, HashState& a,
                                                 HashState& b) {
   a.x = fmix64(ka ^ salt);
@@ -96,19 +97,25 @@ __device__ __forceinline__ void pac_hash_begin2(uint64_t ka, uint64_t kb, uint64
   b.k = (cb > 32) ? (cb - 32) : (32 - cb);
   a.cand = (ca > 32) ? a.x : ~a.x;
   b.cand = (cb > 32) ? b.x : ~b.x;
-  const uint64_t wa = fmix64(a.x ^ kDrawSeed), wb = fmix64(b.x ^ kDrawSeed);
+  a.w0 = fmix64(a.x ^ kDrawSeed);
+  b.w0 = fmix64(b.x ^ kDrawSeed);
 #pragma unroll
   for (int t = 0; t < 10; ++t) {
-    draw_step(wa, t, a.cand, a.k);
-    draw_step(wb, t, b.cand, b.k);
+    draw_step(a.w0, t, a.cand, a.k);
+    draw_step(b.w0, t, b.cand, b.k);
   }
 }
 
+// mask after the draws so far: x with the flipped majority positions toggled
+__device__ __forceinline__ uint64_t hash_mask_now(const HashState& h) {
+  return (__popcll(h.x) > 32) ? h.cand : ~h.cand;
+}
+
 __device__ __forceinline__ uint64_t pac_hash_dev(uint64_t key, uint64_t salt) {
-  HashState h = pac_hash_begin(key, salt);
-  const uint64_t cand0 = (__popcll(h.x) > 32) ? h.x : ~h.x;
-  if (h.k == 0) return h.x ^ (cand0 ^ h.cand);
-  return pac_hash_finish(h.x, h.cand, h.k);
+  const HashState h = pac_hash_begin(key, salt);
+  const uint64_t m = hash_mask_now(h);
+  if (h.k == 0) return m;
+  return pac_hash_continue(m, h.w0);
 }
 
 // ------------------------------------------------------------------ Philox4x32-10 (R13)
