@@ -58,6 +58,19 @@ def _load():
         L.orc_normal.restype = ctypes.c_double
         L.orc_normal.argtypes = [_P]
         L.orc_posterior_update.argtypes = [_P, _P, ctypes.c_double, ctypes.c_double]
+        L.orc_lift.argtypes = [ctypes.c_int, ctypes.c_int64, _P, _P, ctypes.c_double, _P, _P, ctypes.c_double,
+                               _P, _P]
+        L.orc_lift_cmp.argtypes = [ctypes.c_int, ctypes.c_int64, _P, _P, ctypes.c_double, _P, _P,
+                                   ctypes.c_double, _P]
+        L.orc_cmp_bits.restype = ctypes.c_uint64
+        L.orc_cmp_bits.argtypes = [ctypes.c_int, ctypes.c_double, _P, ctypes.c_uint64]
+        L.orc_select.argtypes = [ctypes.c_int64, _P, _P, _P, _P]
+        L.orc_select_cmp.argtypes = [ctypes.c_int, ctypes.c_int64, _P, _P, _P, _P, _P, _P]
+        L.orc_filter.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int64, _P, _P]
+        L.orc_filter_cmp.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_int64, _P, _P,
+                                     _P, _P, _P]
+        L.orc_noised_y.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_int, _P, ctypes.c_int64, _P, _P,
+                                   ctypes.c_uint32, _P, _P, _P]
         L.orc_finalize.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_int, _P, ctypes.c_int64,
                                    ctypes.c_int, _P, _P, _P, _P, _P, ctypes.c_uint32, _P, _P, _P, _P]
         _lib = L
@@ -208,3 +221,100 @@ def finalize(seed: int, B: float, jstar: int, P: np.ndarray, table: dict, round_
                          _ptr(table["K"]), _ptr(table["rows"]), _ptr(table["count"]), wptr,
                          int(round_), _ptr(release), _ptr(is_null), _ptr(flags), _ptr(delta))
     return release, is_null, flags, delta, P
+
+
+# ------------------------------------------------------------------ categorical path (§8 f1)
+OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_MIN, OP_MAX = range(6)
+CMP_LT, CMP_LE, CMP_GT, CMP_GE, CMP_EQ = range(5)
+
+
+def world_vectors(table: dict, a: int):
+    """(y[G,64], presence[G]) of aggregate a of every group (R22)."""
+    G = table["G"]
+    y = np.stack([y_vector(table, a, g) for g in range(G)]) if G else np.zeros((0, M))
+    return y, np.array(table["K"], dtype=np.uint64).copy()
+
+
+def _vec(x):
+    """(pointer to y or None, pointer to presence or None, scalar) of a lift operand:
+    a (y, presence) pair or a Python scalar."""
+    if isinstance(x, tuple):
+        y = np.ascontiguousarray(x[0], dtype=np.float64)
+        p = np.ascontiguousarray(x[1], dtype=np.uint64)
+        return y, p, 0.0
+    return None, None, float(x)
+
+
+def lift(op: int, a, b, n: int):
+    ya, pa, sa = _vec(a)
+    yb, pb, sb = _vec(b)
+    out = np.zeros((n, M), dtype=np.float64)
+    pout = np.zeros(n, dtype=np.uint64)
+    _load().orc_lift(op, n, _ptr(ya), _ptr(pa), sa, _ptr(yb), _ptr(pb), sb, _ptr(out), _ptr(pout))
+    return out, pout
+
+
+def lift_cmp(cmp: int, a, b, n: int) -> np.ndarray:
+    ya, pa, sa = _vec(a)
+    yb, pb, sb = _vec(b)
+    bits = np.zeros(n, dtype=np.uint64)
+    _load().orc_lift_cmp(cmp, n, _ptr(ya), _ptr(pa), sa, _ptr(yb), _ptr(pb), sb, _ptr(bits))
+    return bits
+
+
+def cmp_bits(cmp: int, v: float, c: np.ndarray, presence: int) -> int:
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    return int(_load().orc_cmp_bits(cmp, float(v), _ptr(c), presence & 0xFFFFFFFFFFFFFFFF))
+
+
+def select(h: np.ndarray, gidx: np.ndarray, bits: np.ndarray) -> np.ndarray:
+    h = np.ascontiguousarray(h, dtype=np.uint64)
+    gidx = np.ascontiguousarray(gidx, dtype=np.int32)
+    bits = np.ascontiguousarray(bits, dtype=np.uint64)
+    out = np.zeros(len(h), dtype=np.uint64)
+    _load().orc_select(len(h), _ptr(h), _ptr(gidx), _ptr(bits), _ptr(out))
+    return out
+
+
+def select_cmp(cmp: int, h, v, gidx, c, presence) -> np.ndarray:
+    h = np.ascontiguousarray(h, dtype=np.uint64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    gidx = np.ascontiguousarray(gidx, dtype=np.int32)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    presence = np.ascontiguousarray(presence, dtype=np.uint64)
+    out = np.zeros(len(h), dtype=np.uint64)
+    _load().orc_select_cmp(cmp, len(h), _ptr(h), _ptr(v), _ptr(gidx), _ptr(c), _ptr(presence), _ptr(out))
+    return out
+
+
+def pac_filter(seed: int, round_: int, bits) -> np.ndarray:
+    bits = np.ascontiguousarray(bits, dtype=np.uint64)
+    out = np.zeros(len(bits), dtype=np.uint8)
+    _load().orc_filter(seed & 0xFFFFFFFFFFFFFFFF, round_, len(bits), _ptr(bits), _ptr(out))
+    return out
+
+
+def filter_cmp(seed: int, round_: int, cmp: int, v, gidx, c, presence) -> np.ndarray:
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    gidx = np.ascontiguousarray(gidx, dtype=np.int32)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    presence = np.ascontiguousarray(presence, dtype=np.uint64)
+    out = np.zeros(len(v), dtype=np.uint8)
+    _load().orc_filter_cmp(seed & 0xFFFFFFFFFFFFFFFF, round_, cmp, len(v), _ptr(v), _ptr(gidx), _ptr(c),
+                           _ptr(presence), _ptr(out))
+    return out
+
+
+def noised_y(seed: int, B: float, jstar: int, P: np.ndarray, y: np.ndarray, presence: np.ndarray,
+             round_: int = 0):
+    """pac_noised of given world vectors (R24).  Returns (release[n], is_null[n], delta[n], P_after)."""
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    presence = np.ascontiguousarray(presence, dtype=np.uint64)
+    n = len(presence)
+    P = np.array(P, dtype=np.float64, copy=True)
+    release = np.zeros(n, dtype=np.float64)
+    is_null = np.zeros(n, dtype=np.uint8)
+    delta = np.zeros(n, dtype=np.float64)
+    _load().orc_noised_y(seed & 0xFFFFFFFFFFFFFFFF, float(B), int(jstar), _ptr(P), n, _ptr(y), _ptr(presence),
+                         int(round_), _ptr(release), _ptr(is_null), _ptr(delta))
+    return release, is_null, delta, P

@@ -25,6 +25,9 @@
  *   finalize        closed forms (single-PU group, y_j=j, constant y), NULL rate,
  *                   noise std, numpy weighted variance, scipy Gaussian Bayes     pinned
  *   posterior       scipy.stats.norm likelihood Bayes update                    pinned
+ *   categorical     (R22-R26) cmp bits == numpy comparisons, select truth table,
+ *   path            filter rates popcount/64 (binomial), lift identities,
+ *                   noised_y closed forms, noise-once beats noise-twice pinned
  */
 #include <math.h>
 #include <stdint.h>
@@ -63,7 +66,7 @@ static void philox_block(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t c2, u
   orc_philox4x32_10(ctr, key, out);
 }
 
-enum { TAG_CELL = 0, TAG_JSTAR = 1, TAG_SALT = 2 }; /* DESIGN.md R13 */
+enum { TAG_CELL = 0, TAG_JSTAR = 1, TAG_SALT = 2, TAG_LIFT = 3, TAG_FILTER = 4 }; /* R13, R24, R25 */
 
 /* ------------------------------------------------------------------ fmix64
  * DESIGN.md R1: the base hash the paper wraps ("We wrap DuckDB's hash function",
@@ -471,5 +474,146 @@ void orc_finalize(uint64_t seed, double B, int jstar, double P[64], int64_t G, i
       release[cell] = yt;
       orc_posterior_update(P, y, yt, delta);
     }
+  }
+}
+
+/* ------------------------------------------------------------------ categorical path
+ * (§8 f1; §3 "pac_filter" / "pac_select", §4 vector-lifted
+ * expressions, §6 the ratio lambda; readings DESIGN.md R22-R26.)
+ *
+ * A world vector is (y[64], presence): y in the released scale (orc_y_vector, R7/R9:
+ * absent worlds read 0), presence = K of the group (R22). */
+
+enum { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_DIV = 3, OP_MIN = 4, OP_MAX = 5 };
+enum { CMP_LT = 0, CMP_LE = 1, CMP_GT = 2, CMP_GE = 3, CMP_EQ = 4 };
+
+static double lift_op(int op, double a, double b) {
+  switch (op) {
+    case OP_ADD: return a + b;
+    case OP_SUB: return a - b;
+    case OP_MUL: return a * b;
+    case OP_DIV: return a / b;
+    case OP_MIN: return fmin(a, b);
+    default: return fmax(a, b);
+  }
+}
+
+/* R23 (Eq. vectorexpressionlambda): out_j = e(a_j, b_j), pointwise; a
+ * NULL vector operand is the scalar broadcast to every world (presence: all worlds);
+ * out presence = AND of the operands' presences; an absent world of the output
+ * holds 0 (R9). */
+void orc_lift(int op, int64_t n, const double* a, const uint64_t* pa, double sa, const double* b,
+              const uint64_t* pb, double sb, double* out, uint64_t* pout) {
+  for (int64_t i = 0; i < n; i++) {
+    uint64_t pres = (a ? pa[i] : ~0ull) & (b ? pb[i] : ~0ull);
+    pout[i] = pres;
+    for (int j = 0; j < ORC_M; j++) {
+      double x = a ? a[i * ORC_M + j] : sa;
+      double y = b ? b[i * ORC_M + j] : sb;
+      out[i * ORC_M + j] = ((pres >> j) & 1u) ? lift_op(op, x, y) : 0.0;
+    }
+  }
+}
+
+static int cmp_holds(int cmp, double v, double c) {
+  switch (cmp) {
+    case CMP_LT: return v < c;
+    case CMP_LE: return v <= c;
+    case CMP_GT: return v > c;
+    case CMP_GE: return v >= c;
+    default: return v == c;
+  }
+}
+
+/* R26: b_j = [present_j and (v cmp c_j)] -- an absent world has no value, and a
+ * comparison with it is NULL, i.e. false in a filter. */
+uint64_t orc_cmp_bits(int cmp, double v, const double c[64], uint64_t presence) {
+  uint64_t b = 0;
+  for (int j = 0; j < ORC_M; j++)
+    if (((presence >> j) & 1u) && cmp_holds(cmp, v, c[j])) b |= 1ull << j;
+  return b;
+}
+
+/* Lifted comparison of two world vectors (or a vector and a broadcast scalar):
+ * bit j = [present_j and (a_j cmp b_j)], present = AND of the presences (R23, R26). */
+void orc_lift_cmp(int cmp, int64_t n, const double* a, const uint64_t* pa, double sa, const double* b,
+                  const uint64_t* pb, double sb, uint64_t* bits) {
+  for (int64_t i = 0; i < n; i++) {
+    uint64_t pres = (a ? pa[i] : ~0ull) & (b ? pb[i] : ~0ull), r = 0;
+    for (int j = 0; j < ORC_M; j++) {
+      double x = a ? a[i * ORC_M + j] : sa;
+      double y = b ? b[i * ORC_M + j] : sb;
+      if (((pres >> j) & 1u) && cmp_holds(cmp, x, y)) r |= 1ull << j;
+    }
+    bits[i] = r;
+  }
+}
+
+/* pac_select (Eq. pac-select): h' = h AND b, b the world booleans of the
+ * row's group (gidx). */
+void orc_select(int64_t n, const uint64_t* h, const int32_t* gidx, const uint64_t* bits, uint64_t* out) {
+  for (int64_t i = 0; i < n; i++) out[i] = h[i] & bits[gidx[i]];
+}
+
+/* pac_select_<cmp>: h' = h AND b with b_j = [v cmp c_j] against the
+ * world vector of the row's group. */
+void orc_select_cmp(int cmp, int64_t n, const uint64_t* h, const double* v, const int32_t* gidx,
+                    const double* c, const uint64_t* pres, uint64_t* out) {
+  for (int64_t i = 0; i < n; i++)
+    out[i] = h[i] & orc_cmp_bits(cmp, v[i], c + (int64_t)gidx[i] * ORC_M, pres[gidx[i]]);
+}
+
+/* pac_filter (Eq. pac-filter): true with probability popcount(b)/m.
+ * R25: r = x0 >> 26 in [0,64) of Philox(seed; i_lo, i_hi, round, TAG_FILTER);
+ * true iff r < popcount(b) -- exactly popcount(b)/64. */
+void orc_filter(uint64_t seed, uint32_t round, int64_t n, const uint64_t* bits, uint8_t* out) {
+  for (int64_t i = 0; i < n; i++) {
+    uint32_t x[4];
+    philox_block(seed, (uint32_t)i, (uint32_t)((uint64_t)i >> 32), round, TAG_FILTER, x);
+    out[i] = (uint8_t)((int)(x[0] >> 26) < popcount64(bits[i]) ? 1 : 0);
+  }
+}
+
+/* pac_filter_<cmp>: pac_filter of b_j = [v cmp c_j]. */
+void orc_filter_cmp(uint64_t seed, uint32_t round, int cmp, int64_t n, const double* v, const int32_t* gidx,
+                    const double* c, const uint64_t* pres, uint8_t* out) {
+  for (int64_t i = 0; i < n; i++) {
+    uint64_t b = orc_cmp_bits(cmp, v[i], c + (int64_t)gidx[i] * ORC_M, pres[gidx[i]]);
+    uint32_t x[4];
+    philox_block(seed, (uint32_t)i, (uint32_t)((uint64_t)i >> 32), round, TAG_FILTER, x);
+    out[i] = (uint8_t)((int)(x[0] >> 26) < popcount64(b) ? 1 : 0);
+  }
+}
+
+/* pac_noised of given world vectors (R24; P:L841-850 applied to a vector-lifted
+ * expression, "gets noised once"): cells i = 0..n-1 in order, y already in the
+ * released scale (no *2), absent worlds read 0 (R9), Philox(seed; i_lo, i_hi, round,
+ * TAG_LIFT), then exactly the per-cell steps of orc_finalize. */
+void orc_noised_y(uint64_t seed, double B, int jstar, double P[64], int64_t n, const double* yv,
+                  const uint64_t* presence, uint32_t round, double* release, uint8_t* is_null,
+                  double* delta_out) {
+  double y[64];
+  for (int64_t i = 0; i < n; i++) {
+    int pc = popcount64(presence[i]);
+    uint32_t x[4];
+    philox_block(seed, (uint32_t)i, (uint32_t)((uint64_t)i >> 32), round, TAG_LIFT, x);
+    if ((int)(x[0] >> 26) >= pc) {
+      is_null[i] = 1;
+      release[i] = NAN;
+      if (delta_out) delta_out[i] = NAN;
+      continue;
+    }
+    is_null[i] = 0;
+    for (int j = 0; j < ORC_M; j++) y[j] = ((presence[i] >> j) & 1u) ? yv[i * ORC_M + j] : 0.0;
+    double s2 = orc_weighted_var(P, y);
+    double delta = s2 / (2.0 * B);
+    if (delta_out) delta_out[i] = delta;
+    if (s2 == 0.0) {
+      release[i] = y[jstar];
+      continue;
+    }
+    double yt = y[jstar] + sqrt(delta) * orc_normal(x);
+    release[i] = yt;
+    orc_posterior_update(P, y, yt, delta);
   }
 }
