@@ -199,6 +199,64 @@ int pac_finalize(pac_session* s, const pac_table* t, const pac_agg_spec* aggs, i
 int pac_posterior_update(pac_session* s, const double* d_y64, double y_tilde, double delta,
                          pac_stream_t stream);
 
+/* ------------------------------------------------------------------ categorical path (§8 f1)
+ * After the aggregate (§3, §4; R22-R26).
+ * A world vector is y[64] (double, released scale, absent worlds 0) plus a presence mask
+ * (uint64, bit j = world j present).  Arrays of n vectors are [n][64] doubles + [n]
+ * presences.  A pac_wvec operand with d_y == NULL is the broadcast scalar `scalar`
+ * (present in every world). */
+typedef enum {
+  PAC_OP_ADD = 0, PAC_OP_SUB = 1, PAC_OP_MUL = 2, PAC_OP_DIV = 3, PAC_OP_MIN = 4, PAC_OP_MAX = 5
+} pac_lift_op;
+typedef enum { PAC_CMP_LT = 0, PAC_CMP_LE = 1, PAC_CMP_GT = 2, PAC_CMP_GE = 3, PAC_CMP_EQ = 4 } pac_cmp_kind;
+typedef struct {
+  const double* d_y;          /* [n][64], or NULL for a scalar */
+  const uint64_t* d_presence; /* [n]; required iff d_y != NULL */
+  double scalar;
+} pac_wvec;
+#define PAC_CMP_INDEX_WORDS 130 /* per group: 64 sorted doubles, 65 suffix masks, count */
+
+/* R22: world vector of aggregate a of every group of table t (the y-vector pac_finalize
+ * noises: 2*count | 2*sum | fsum/count | ext, absent worlds 0) into d_y [G_cap][64], and
+ * its presence K into d_presence [G_cap].  Rows >= num_groups get zeros / presence 0. */
+int pac_world_vector(const pac_table* t, const pac_agg_spec* aggs, int n_aggs, int a, int64_t G_cap,
+                     double* d_y, uint64_t* d_presence, pac_stream_t stream);
+/* R23 (Eq. vectorexpressionlambda): d_out[i][j] = a_ij OP b_ij where both
+ * operands are present, else 0; d_presence_out[i] = presence(a) AND presence(b). */
+int pac_lift(int op, const pac_wvec* a, const pac_wvec* b, int64_t n, double* d_out,
+             uint64_t* d_presence_out, pac_stream_t stream);
+/* Lifted comparison: d_bits[i] bit j = present_j and (a_ij CMP b_ij) (R23, R26). */
+int pac_lift_cmp(int cmp, const pac_wvec* a, const pac_wvec* b, int64_t n, uint64_t* d_bits,
+                 pac_stream_t stream);
+/* R24: pac_noised of n given world vectors, cells in index order i, Philox counter
+ * (i_lo, i_hi, round, 3): NULL with probability (64 - popcount(presence))/64, y already in
+ * the released scale (no *2), then the pac_finalize steps (variance under P, release,
+ * Bayesian update of the session posterior).  d_delta may be NULL. */
+int pac_noised_y_workspace_size(int64_t n, size_t* bytes);
+int pac_noised_y(pac_session* s, const double* d_y, const uint64_t* d_presence, int64_t n, uint32_t round,
+                 double* d_release, uint8_t* d_is_null, double* d_delta, void* d_ws, size_t ws_bytes,
+                 pac_stream_t stream);
+/* Comparison index of G world vectors (d_c [G][64], d_presence [G]) for the fused
+ * row-parallel comparisons below: d_index [G][PAC_CMP_INDEX_WORDS] (caller-allocated). */
+int pac_cmp_index(const double* d_c, const uint64_t* d_presence, int64_t G, uint64_t* d_index,
+                  pac_stream_t stream);
+/* pac_select (Eq. pac-select): d_out[i] = d_h[i] AND d_bits[d_gidx[i]] -- the reduced
+ * mask of row i for an upstream PAC aggregate (pass it as pac_agg_grouped's d_mask). */
+int pac_select(const uint64_t* d_h, const int32_t* d_gidx, const uint64_t* d_bits, int64_t n,
+               uint64_t* d_out, pac_stream_t stream);
+/* pac_select_<cmp>: d_out[i] = d_h[i] AND b, b_j = present_j and
+ * (d_v[i] CMP c_j), c = the world vector of group d_gidx[i] in the comparison index. */
+int pac_select_cmp(int cmp, const uint64_t* d_h, const double* d_v, const int32_t* d_gidx,
+                   const uint64_t* d_index, int64_t n, uint64_t* d_out, pac_stream_t stream);
+/* pac_filter (Eq. pac-filter; R25): d_out[i] = 1 with probability
+ * popcount(d_bits[i])/64: r = x0 >> 26 of Philox(session seed; i_lo, i_hi, round, 4),
+ * true iff r < popcount. */
+int pac_filter(pac_session* s, const uint64_t* d_bits, int64_t n, uint32_t round, uint8_t* d_out,
+               pac_stream_t stream);
+/* pac_filter_<cmp>: pac_filter of the pac_select_cmp booleans. */
+int pac_filter_cmp(pac_session* s, int cmp, const double* d_v, const int32_t* d_gidx, const uint64_t* d_index,
+                   int64_t n, uint32_t round, uint8_t* d_out, pac_stream_t stream);
+
 /* ------------------------------------------------------------------ runtime / profiling
  * Number of kernels this library has launched since load (all entry points). */
 uint64_t pac_launch_count(void);

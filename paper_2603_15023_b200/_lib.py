@@ -32,6 +32,15 @@ class KeyCol(ctypes.Structure):
     _fields_ = [("d_col", ctypes.c_void_p), ("elem_bytes", ctypes.c_int32)]
 
 
+class WVec(ctypes.Structure):
+    _fields_ = [("d_y", ctypes.c_void_p), ("d_presence", ctypes.c_void_p), ("scalar", ctypes.c_double)]
+
+
+OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_MIN, OP_MAX = range(6)
+CMP_LT, CMP_LE, CMP_GT, CMP_GE, CMP_EQ = range(5)
+PAC_CMP_INDEX_WORDS = 130
+
+
 class Table(ctypes.Structure):
     _fields_ = [("d_num_groups", ctypes.c_void_p), ("d_status", ctypes.c_void_p),
                 ("d_group_key", ctypes.c_void_p), ("d_rows", ctypes.c_void_p),
@@ -68,6 +77,17 @@ def lib() -> ctypes.CDLL:
         "pac_finalize": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32, _P, _P, _P,
                                         _P, _P, ctypes.c_size_t, _P]),
         "pac_posterior_update": (ctypes.c_int, [_P, _P, ctypes.c_double, ctypes.c_double, _P]),
+        "pac_world_vector": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _P, _P, _P]),
+        "pac_lift": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int64, _P, _P, _P]),
+        "pac_lift_cmp": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int64, _P, _P]),
+        "pac_noised_y_workspace_size": (ctypes.c_int, [ctypes.c_int64, _P]),
+        "pac_noised_y": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64, ctypes.c_uint32, _P, _P, _P, _P,
+                                        ctypes.c_size_t, _P]),
+        "pac_cmp_index": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P, _P]),
+        "pac_select": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64, _P, _P]),
+        "pac_select_cmp": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, ctypes.c_int64, _P, _P]),
+        "pac_filter": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_uint32, _P, _P]),
+        "pac_filter_cmp": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int64, ctypes.c_uint32, _P, _P]),
         "pac_launch_count": (ctypes.c_uint64, []),
         "pac_profile_enable": (ctypes.c_int, [ctypes.c_int]),
         "pac_profile_read": (ctypes.c_int, [_P, _P]),
@@ -90,5 +110,7 @@ def exported_symbols() -> list:
     return ["pac_session_create", "pac_session_destroy", "pac_session_query", "pac_session_set_posterior",
             "pac_session_posterior_device", "pac_mask", "pac_agg_workspace_size", "pac_agg_grouped",
             "pac_table_check", "pac_table_rederive_presence", "pac_table_remap",
-            "pac_finalize_workspace_size", "pac_finalize", "pac_posterior_update", "pac_launch_count",
+            "pac_finalize_workspace_size", "pac_finalize", "pac_posterior_update", "pac_world_vector",
+            "pac_lift", "pac_lift_cmp", "pac_noised_y_workspace_size", "pac_noised_y", "pac_cmp_index",
+            "pac_select", "pac_select_cmp", "pac_filter", "pac_filter_cmp", "pac_launch_count",
             "pac_profile_enable", "pac_profile_read", "pac_version"]

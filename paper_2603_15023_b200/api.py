@@ -286,6 +286,141 @@ def posterior_update(session: Session, y64: torch.Tensor, y_tilde: float, delta:
                                                                 float(delta), _stream(y64.device)))
 
 
+# ------------------------------------------------------------------ categorical path (§8 f1)
+# World vectors are (y, presence) pairs: y float64 [n, 64] in the released scale (R22),
+# presence int64 [n] holding the 64-bit masks.  A Python number is a broadcast scalar.
+from ._lib import (CMP_EQ, CMP_GE, CMP_GT, CMP_LE, CMP_LT, OP_ADD, OP_DIV, OP_MAX,  # noqa: E402
+                   OP_MIN, OP_MUL, OP_SUB)
+
+
+def world_vector(table: PacTable, a: int) -> Tuple[torch.Tensor, torch.Tensor]:
+    """pac_world_vector: the y-vectors of aggregate a of every group (R22)."""
+    dev = table.rows.device
+    y = torch.empty(table.G_cap, PAC_M, dtype=torch.float64, device=dev)
+    pres = torch.empty(table.G_cap, dtype=torch.int64, device=dev)
+    specs = _agg_specs([(k, w) for k, w in zip(table.kinds, table.world)])
+    check("pac_world_vector", L.lib().pac_world_vector(ctypes.byref(table.struct()), specs, len(table.kinds), a,
+                                                        table.G_cap, _ptr(y), _ptr(pres), _stream(dev)))
+    return y, pres
+
+
+def _wvec(x):
+    w = L.WVec()
+    if isinstance(x, tuple):
+        y, p = x
+        _require_cuda(y, p)
+        w.d_y, w.d_presence, w.scalar = y.data_ptr(), p.data_ptr(), 0.0
+        return w, y.shape[0], y.device
+    w.d_y, w.d_presence, w.scalar = None, None, float(x)
+    return w, None, None
+
+
+def _operands(a, b):
+    wa, na, da = _wvec(a)
+    wb, nb, db = _wvec(b)
+    n = na if na is not None else nb
+    if n is None:
+        raise ValueError("at least one operand must be a world vector")
+    if na is not None and nb is not None and na != nb:
+        raise ValueError("world vector operands differ in length")
+    return wa, wb, n, da if da is not None else db
+
+
+def lift(op: int, a, b) -> Tuple[torch.Tensor, torch.Tensor]:
+    """pac_lift: pointwise a OP b over world vectors / broadcast scalars (R23)."""
+    wa, wb, n, dev = _operands(a, b)
+    out = torch.empty(n, PAC_M, dtype=torch.float64, device=dev)
+    pres = torch.empty(n, dtype=torch.int64, device=dev)
+    check("pac_lift", L.lib().pac_lift(int(op), ctypes.byref(wa), ctypes.byref(wb), n, _ptr(out), _ptr(pres),
+                                        _stream(dev)))
+    return out, pres
+
+
+def lift_cmp(cmp: int, a, b) -> torch.Tensor:
+    """pac_lift_cmp: world booleans (int64 bit patterns) of a CMP b (R23, R26)."""
+    wa, wb, n, dev = _operands(a, b)
+    bits = torch.empty(n, dtype=torch.int64, device=dev)
+    check("pac_lift_cmp", L.lib().pac_lift_cmp(int(cmp), ctypes.byref(wa), ctypes.byref(wb), n, _ptr(bits),
+                                                _stream(dev)))
+    return bits
+
+
+class NoisedY:
+    """pac_noised_y with a cached workspace (R24)."""
+
+    def __init__(self, n: int, device="cuda"):
+        self.n = int(n)
+        dev = torch.device(device)
+        nb = ctypes.c_size_t()
+        check("pac_noised_y_workspace_size", L.lib().pac_noised_y_workspace_size(self.n, ctypes.byref(nb)))
+        self.ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=dev)
+        self.ws_bytes = nb.value
+        self.release = torch.empty(self.n, dtype=torch.float64, device=dev)
+        self.is_null = torch.empty(self.n, dtype=torch.uint8, device=dev)
+        self.delta = torch.empty(self.n, dtype=torch.float64, device=dev)
+
+    def __call__(self, session: Session, y: torch.Tensor, presence: torch.Tensor, round_: int = 0):
+        _require_cuda(y, presence)
+        n = presence.numel()
+        if n > self.n:
+            raise ValueError("more vectors than the NoisedY capacity")
+        check("pac_noised_y", L.lib().pac_noised_y(
+            session.handle, _ptr(y), _ptr(presence), n, int(round_), _ptr(self.release), _ptr(self.is_null),
+            _ptr(self.delta), _ptr(self.ws), self.ws_bytes, _stream(y.device)))
+        return self.release[:n], self.is_null[:n], self.delta[:n]
+
+
+def noised_y(session: Session, y: torch.Tensor, presence: torch.Tensor, round_: int = 0):
+    return NoisedY(presence.numel(), y.device)(session, y, presence, round_)
+
+
+def cmp_index(c: torch.Tensor, presence: torch.Tensor) -> torch.Tensor:
+    """pac_cmp_index: sorted world values + suffix masks per group, for select_cmp / filter_cmp."""
+    _require_cuda(c, presence)
+    G = presence.numel()
+    ix = torch.empty(G, L.PAC_CMP_INDEX_WORDS, dtype=torch.int64, device=c.device)
+    check("pac_cmp_index", L.lib().pac_cmp_index(_ptr(c), _ptr(presence), G, _ptr(ix), _stream(c.device)))
+    return ix
+
+
+def select(h: torch.Tensor, gidx: torch.Tensor, bits: torch.Tensor, out: Optional[torch.Tensor] = None):
+    """pac_select: h AND bits[gidx] (Eq. pac-select) -- reduced masks for an upstream aggregate."""
+    _require_cuda(h, gidx, bits)
+    out = torch.empty_like(h) if out is None else out
+    check("pac_select", L.lib().pac_select(_ptr(h), _ptr(gidx), _ptr(bits), h.numel(), _ptr(out),
+                                            _stream(h.device)))
+    return out
+
+
+def select_cmp(cmp: int, h: torch.Tensor, v: torch.Tensor, gidx: torch.Tensor, index: torch.Tensor,
+               out: Optional[torch.Tensor] = None):
+    """pac_select_<cmp>: h AND [v CMP c_j] against the row group's world vector."""
+    _require_cuda(h, v, gidx, index)
+    out = torch.empty_like(h) if out is None else out
+    check("pac_select_cmp", L.lib().pac_select_cmp(int(cmp), _ptr(h), _ptr(v), _ptr(gidx), _ptr(index), h.numel(),
+                                                    _ptr(out), _stream(h.device)))
+    return out
+
+
+def pac_filter(session: Session, bits: torch.Tensor, round_: int = 0) -> torch.Tensor:
+    """pac_filter: 1 with probability popcount(b)/64 (Eq. pac-filter, R25)."""
+    _require_cuda(bits)
+    out = torch.empty(bits.numel(), dtype=torch.uint8, device=bits.device)
+    check("pac_filter", L.lib().pac_filter(session.handle, _ptr(bits), bits.numel(), int(round_), _ptr(out),
+                                            _stream(bits.device)))
+    return out
+
+
+def filter_cmp(session: Session, cmp: int, v: torch.Tensor, gidx: torch.Tensor, index: torch.Tensor,
+               round_: int = 0) -> torch.Tensor:
+    """pac_filter_<cmp>: pac_filter of [v CMP c_j]."""
+    _require_cuda(v, gidx, index)
+    out = torch.empty(v.numel(), dtype=torch.uint8, device=v.device)
+    check("pac_filter_cmp", L.lib().pac_filter_cmp(session.handle, int(cmp), _ptr(v), _ptr(gidx), _ptr(index),
+                                                    v.numel(), int(round_), _ptr(out), _stream(v.device)))
+    return out
+
+
 # ------------------------------------------------------------------ runtime
 def launch_count() -> int:
     return int(L.lib().pac_launch_count())

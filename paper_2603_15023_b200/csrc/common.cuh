@@ -140,7 +140,7 @@ __host__ __device__ __forceinline__ u32x4 philox4x32_10(u32x4 c, uint32_t k0, ui
   return c;
 }
 
-enum { kTagCell = 0, kTagJstar = 1, kTagSalt = 2 };
+enum { kTagCell = 0, kTagJstar = 1, kTagSalt = 2, kTagLift = 3, kTagFilter = 4 };  // R13, R24, R25
 
 // ------------------------------------------------------------------ ordered f64 <-> int64
 // Monotone map of doubles onto signed int64, so MIN/MAX become atomicMin/atomicMax.

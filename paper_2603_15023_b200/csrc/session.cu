@@ -106,6 +106,29 @@ __global__ void k_finalize_prep(FinPrep f) {
   }
 }
 
+// pac_noised_y prep (R24): one warp per given world vector -- Philox block with TAG_LIFT,
+// NULL decision from popcount(presence) (R10), normal draw, y copied with absent worlds 0 (R9).
+__global__ void k_noised_prep_y(const double* __restrict__ y, const uint64_t* __restrict__ presence, int64_t n,
+                                uint64_t seed, uint32_t round, double* ybuf, double* zbuf, uint8_t* is_null) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
+    const uint64_t pr = presence[i];
+    const u32x4 x = philox4x32_10({(uint32_t)i, (uint32_t)((uint64_t)i >> 32), round, kTagLift},
+                                  (uint32_t)seed, (uint32_t)(seed >> 32));
+    const bool null = (int)(x.x >> 26) >= __popcll(pr);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h;
+      ybuf[i * kM + j] = ((pr >> j) & 1ull) ? y[i * kM + j] : 0.0;
+    }
+    if (lane == 0) {
+      is_null[i] = null ? 1 : 0;
+      zbuf[i] = null ? 0.0 : normal_from(x);
+    }
+  }
+}
+
 // P <- P*W / sum(P*W) over worlds with P_j > 0 (R14); lane owns j, j+32
 __device__ __forceinline__ void bayes_update(double& p0, double& p1, double y0, double y1, double yt,
                                              double delta) {
@@ -121,6 +144,7 @@ __device__ __forceinline__ void bayes_update(double& p0, double& p1, double y0, 
 }
 
 // one warp: the sequential release chain
+// num_groups == nullptr: G_cap cells-per-aggregate rows are all valid (pac_noised_y)
 __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups, int64_t G_cap, int A,
                                                        const double* __restrict__ ybuf,
                                                        const double* __restrict__ zbuf,
@@ -128,7 +152,7 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
                                                        unsigned long long* releases, int jstar, double B,
                                                        double* release, double* delta_out) {
   const int lane = threadIdx.x;
-  const int64_t G = min(*num_groups, G_cap);
+  const int64_t G = num_groups ? min(*num_groups, G_cap) : G_cap;
   const int64_t cells = G * A;
   double p0 = P[lane], p1 = P[lane + 32];
   unsigned long long nrel = 0;
@@ -204,6 +228,8 @@ static size_t fin_ws(int64_t G_cap, int A, size_t* o_z, size_t* o_n) {
   *o_n = (*o_z + z + 255) & ~(size_t)255;
   return *o_n + cells + 256;
 }
+
+uint64_t session_seed(const pac_session* s) { return s->seed; }
 
 }  // namespace pac
 
@@ -324,6 +350,34 @@ extern "C" int pac_posterior_update(pac_session* s, const double* d_y64, double 
                                     pac_stream_t stream) {
   if (!s || !d_y64 || !(delta > 0.0) || !std::isfinite(delta) || !std::isfinite(y_tilde)) return PAC_E_INVAL;
   k_posterior_update<<<1, 32, 0, (cudaStream_t)stream>>>(s->d_P, d_y64, y_tilde, delta);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
+}
+
+extern "C" int pac_noised_y_workspace_size(int64_t n, size_t* bytes) {
+  if (!bytes || n < 0) return PAC_E_INVAL;
+  size_t oz, on;
+  *bytes = fin_ws(n > 0 ? n : 1, 1, &oz, &on);
+  return PAC_OK;
+}
+
+extern "C" int pac_noised_y(pac_session* s, const double* d_y, const uint64_t* d_presence, int64_t n, uint32_t round,
+                            double* d_release, uint8_t* d_is_null, double* d_delta, void* d_ws, size_t ws_bytes,
+                            pac_stream_t stream) {
+  if (!s || n < 0 || (n > 0 && (!d_y || !d_presence || !d_release || !d_is_null))) return PAC_E_INVAL;
+  if (n == 0) return PAC_OK;
+  size_t oz, on;
+  const size_t need = fin_ws(n, 1, &oz, &on);
+  if (!d_ws || ws_bytes < need) return PAC_E_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = (char*)d_ws;
+  double* ybuf = (double*)ws;
+  double* zbuf = (double*)(ws + oz);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, 148 * 32));
+  k_noised_prep_y<<<blocks, 256, 0, st>>>(d_y, d_presence, n, s->seed, round, ybuf, zbuf, d_is_null);
+  note_launch();
+  k_finalize_chain<<<1, 32, 0, st>>>(nullptr, n, 1, ybuf, zbuf, d_is_null, s->d_P, s->d_count, s->jstar, s->B,
+                                     d_release, d_delta);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
