@@ -69,6 +69,7 @@ def _load():
         L.orc_filter.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int64, _P, _P]
         L.orc_filter_cmp.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_int64, _P, _P,
                                      _P, _P, _P]
+        L.orc_join_chain_mask.argtypes = [ctypes.c_int, _P, _P, _P, _P, ctypes.c_int64, ctypes.c_uint64, _P, _P, _P]
         L.orc_noised_y.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_int, _P, ctypes.c_int64, _P, _P,
                                    ctypes.c_uint32, _P, _P, _P]
         L.orc_finalize.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_int, _P, ctypes.c_int64,
@@ -318,3 +319,22 @@ def noised_y(seed: int, B: float, jstar: int, P: np.ndarray, y: np.ndarray, pres
     _load().orc_noised_y(seed & 0xFFFFFFFFFFFFFFFF, float(B), int(jstar), _ptr(P), n, _ptr(y), _ptr(presence),
                          int(round_), _ptr(release), _ptr(is_null), _ptr(delta))
     return release, is_null, delta, P
+
+
+# ------------------------------------------------------------------ PU-key join (§8 f2)
+def join_chain_mask(tables, fk: np.ndarray, salt: int):
+    """tables: [(pk, next)] along the FK chain (R27).  Returns (mask, found, pu_key)."""
+    k = len(tables)
+    pks = [np.ascontiguousarray(t[0], dtype=np.int64) for t in tables]
+    nxt = [np.ascontiguousarray(t[1], dtype=np.int64) for t in tables]
+    pk_p = (ctypes.c_void_p * max(1, k))(*[a.ctypes.data for a in pks])
+    nx_p = (ctypes.c_void_p * max(1, k))(*[a.ctypes.data for a in nxt])
+    nb = np.array([len(a) for a in pks], dtype=np.int64)
+    fk = np.ascontiguousarray(fk, dtype=np.int64)
+    n = len(fk)
+    mask = np.zeros(n, dtype=np.uint64)
+    found = np.zeros(n, dtype=np.uint8)
+    pu = np.zeros(n, dtype=np.int64)
+    _load().orc_join_chain_mask(k, pk_p, nx_p, _ptr(nb), _ptr(fk), n, salt & 0xFFFFFFFFFFFFFFFF, _ptr(mask),
+                                _ptr(found), _ptr(pu))
+    return mask, found, pu

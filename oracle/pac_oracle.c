@@ -617,3 +617,44 @@ void orc_noised_y(uint64_t seed, double B, int jstar, double P[64], int64_t n, c
     orc_posterior_update(P, y, yt, delta);
   }
 }
+
+/* ------------------------------------------------------------------ PU-key join (§8 f2)
+ * P:L331-357 §3 (Eq. join-addition, Eq. join-elim), §2; reading R27.
+ * The chain T -fk1-> T1 -fk2-> ... -> Tk -fkU-> U with join elimination: starting from the
+ * row's fk1, look the key up in T1's primary-key column and continue with that tuple's next
+ * FK, k times; the last FK (Tk.fk_U == U.pk by referential integrity) is the PU key, and
+ * the row's mask is pac_hash(PU key).  A row whose key finds no match has no PU (it would
+ * not survive the inserted inner join): mask 0, found 0.  Lookup = binary search of the
+ * table's (pk, next) pairs sorted by pk (libc qsort/bsearch). */
+typedef struct { int64_t pk, next; } pk_pair;
+static int cmp_pair(const void* a, const void* b) {
+  int64_t x = ((const pk_pair*)a)->pk, y = ((const pk_pair*)b)->pk;
+  return (x > y) - (x < y);
+}
+
+void orc_join_chain_mask(int k, const int64_t* const* pk, const int64_t* const* next, const int64_t* n_build,
+                         const int64_t* fk, int64_t n, uint64_t salt, uint64_t* mask, uint8_t* found,
+                         int64_t* pu) {
+  pk_pair* tab[8];
+  for (int t = 0; t < k; t++) {
+    tab[t] = (pk_pair*)malloc((size_t)(n_build[t] > 0 ? n_build[t] : 1) * sizeof(pk_pair));
+    for (int64_t i = 0; i < n_build[t]; i++) {
+      tab[t][i].pk = pk[t][i];
+      tab[t][i].next = next[t][i];
+    }
+    qsort(tab[t], (size_t)n_build[t], sizeof(pk_pair), cmp_pair);
+  }
+  for (int64_t i = 0; i < n; i++) {
+    int64_t x = fk[i];
+    int ok = 1;
+    for (int t = 0; t < k && ok; t++) {
+      pk_pair key = {x, 0};
+      const pk_pair* hit = (const pk_pair*)bsearch(&key, tab[t], (size_t)n_build[t], sizeof(pk_pair), cmp_pair);
+      if (hit) x = hit->next; else ok = 0;
+    }
+    found[i] = (uint8_t)ok;
+    pu[i] = ok ? x : 0;
+    mask[i] = ok ? orc_pac_hash(x, salt) : 0;
+  }
+  for (int t = 0; t < k; t++) free(tab[t]);
+}
