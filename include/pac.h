@@ -257,6 +257,28 @@ int pac_filter(pac_session* s, const uint64_t* d_bits, int64_t n, uint32_t round
 int pac_filter_cmp(pac_session* s, int cmp, const double* d_v, const int32_t* d_gidx, const uint64_t* d_index,
                    int64_t n, uint32_t round, uint8_t* d_out, pac_stream_t stream);
 
+/* ------------------------------------------------------------------ PU-key join (§8 f2)
+ * P:L331-357 §3 (Eq. join-addition, Eq. join-elim), §2; reading R27.  A build
+ * table maps a primary key to the tuple's next foreign key along the chain
+ * T -fk1-> T1 -> ... -> Tk -fkU-> U (e.g. orders: o_orderkey -> o_custkey).  The table is a
+ * caller-allocated device buffer of pac_join_table_bytes(n_build) bytes (16-byte aligned):
+ * open addressing, load factor <= 1/2, 16-byte {key, next} slots. */
+#define PAC_JOIN_MAX_CHAIN 4
+int pac_join_table_bytes(int64_t n_build, size_t* bytes);
+/* Builds the table from d_pk[n_build] -> d_next[n_build].  A duplicate primary key is
+ * recorded in the table status (PAC_E_INVAL) -- see pac_join_table_status. */
+int pac_join_build(const int64_t* d_pk, const int64_t* d_next, int64_t n_build, void* d_table,
+                   size_t table_bytes, pac_stream_t stream);
+/* Synchronizing: PAC_OK, or PAC_E_INVAL if the build saw a duplicate primary key. */
+int pac_join_table_status(const void* d_table, pac_stream_t stream);
+/* Per row i: x = d_fk[i]; for t = 0..k-1: x = next of x in table t (k <= PAC_JOIN_MAX_CHAIN;
+ * d_tables is a HOST array of k device table pointers).  Join elimination (Eq. join-elim):
+ * the final x is the PU key; d_mask[i] = pac_hash(x, salt) (R1, R2), or 0 when some lookup
+ * finds no match (R27: no PU -> in no world; pac_agg_grouped drops the row, R21).  Either
+ * output may be NULL (d_pu_key[i] = x, or 0 without a match). */
+int pac_join_mask(const void* const* d_tables, int k, const int64_t* d_fk, int64_t n, uint64_t salt,
+                  uint64_t* d_mask, int64_t* d_pu_key, pac_stream_t stream);
+
 /* ------------------------------------------------------------------ runtime / profiling
  * Number of kernels this library has launched since load (all entry points). */
 uint64_t pac_launch_count(void);

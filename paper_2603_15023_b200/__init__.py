@@ -9,3 +9,4 @@ from .api import (Aggregator, Finalizer, PacTable, Session, agg_grouped, as_u64,
 from .api import (CMP_EQ, CMP_GE, CMP_GT, CMP_LE, CMP_LT, OP_ADD, OP_DIV, OP_MAX, OP_MIN, OP_MUL,  # noqa: F401
                   OP_SUB, NoisedY, cmp_index, filter_cmp, lift, lift_cmp, noised_y, pac_filter, select,
                   select_cmp, world_vector)
+from .api import JoinTable, join_mask  # noqa: F401

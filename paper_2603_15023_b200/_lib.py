@@ -88,6 +88,10 @@ def lib() -> ctypes.CDLL:
         "pac_select_cmp": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, ctypes.c_int64, _P, _P]),
         "pac_filter": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_uint32, _P, _P]),
         "pac_filter_cmp": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int64, ctypes.c_uint32, _P, _P]),
+        "pac_join_table_bytes": (ctypes.c_int, [ctypes.c_int64, _P]),
+        "pac_join_build": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P, ctypes.c_size_t, _P]),
+        "pac_join_table_status": (ctypes.c_int, [_P, _P]),
+        "pac_join_mask": (ctypes.c_int, [_P, ctypes.c_int, _P, ctypes.c_int64, ctypes.c_uint64, _P, _P, _P]),
         "pac_launch_count": (ctypes.c_uint64, []),
         "pac_profile_enable": (ctypes.c_int, [ctypes.c_int]),
         "pac_profile_read": (ctypes.c_int, [_P, _P]),
@@ -112,5 +116,6 @@ def exported_symbols() -> list:
             "pac_table_check", "pac_table_rederive_presence", "pac_table_remap",
             "pac_finalize_workspace_size", "pac_finalize", "pac_posterior_update", "pac_world_vector",
             "pac_lift", "pac_lift_cmp", "pac_noised_y_workspace_size", "pac_noised_y", "pac_cmp_index",
-            "pac_select", "pac_select_cmp", "pac_filter", "pac_filter_cmp", "pac_launch_count",
+            "pac_select", "pac_select_cmp", "pac_filter", "pac_filter_cmp", "pac_join_table_bytes",
+            "pac_join_build", "pac_join_table_status", "pac_join_mask", "pac_launch_count",
             "pac_profile_enable", "pac_profile_read", "pac_version"]

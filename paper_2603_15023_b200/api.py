@@ -421,6 +421,37 @@ def filter_cmp(session: Session, cmp: int, v: torch.Tensor, gidx: torch.Tensor, 
     return out
 
 
+# ------------------------------------------------------------------ PU-key join (§8 f2)
+class JoinTable:
+    """pac_join_build: primary key -> next foreign key of one table on the FK chain (R27)."""
+
+    def __init__(self, pk: torch.Tensor, nxt: torch.Tensor):
+        _require_cuda(pk, nxt)
+        if pk.dtype != torch.int64 or nxt.dtype != torch.int64 or pk.numel() != nxt.numel():
+            raise ValueError("pk and next must be int64 tensors of one length")
+        nb = ctypes.c_size_t()
+        check("pac_join_table_bytes", L.lib().pac_join_table_bytes(pk.numel(), ctypes.byref(nb)))
+        self.buf = torch.empty((nb.value + 15) // 16 * 2, dtype=torch.int64, device=pk.device)
+        self.nbytes = nb.value
+        check("pac_join_build", L.lib().pac_join_build(_ptr(pk), _ptr(nxt), pk.numel(), _ptr(self.buf),
+                                                        self.nbytes, _stream(pk.device)))
+
+    def status(self) -> int:
+        return int(L.lib().pac_join_table_status(_ptr(self.buf), _stream(self.buf.device)))
+
+
+def join_mask(tables: Sequence[JoinTable], fk: torch.Tensor, salt: int, want_pu: bool = False):
+    """pac_join_mask: masks of the rows' PU keys reached along the FK chain (join elimination)."""
+    _require_cuda(fk)
+    k = len(tables)
+    arr = (ctypes.c_void_p * max(1, k))(*[t.buf.data_ptr() for t in tables])
+    mask = torch.empty_like(fk)
+    pu = torch.empty_like(fk) if want_pu else None
+    check("pac_join_mask", L.lib().pac_join_mask(arr, k, _ptr(fk), fk.numel(), salt & 0xFFFFFFFFFFFFFFFF,
+                                                  _ptr(mask), _ptr(pu), _stream(fk.device)))
+    return (mask, pu) if want_pu else mask
+
+
 # ------------------------------------------------------------------ runtime
 def launch_count() -> int:
     return int(L.lib().pac_launch_count())
