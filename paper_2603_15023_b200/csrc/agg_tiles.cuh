@@ -672,9 +672,11 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
       misc->nonfinite = 0;
     }
   }
-  __syncthreads();
-  // ---------------- B3: unit positions, zero padding rows, run descriptors
-  for (int s = tid; s < Lcap; s += nth) {
+  // ---------------- B3: unit positions, zero padding rows, run descriptors.  With at most 32
+  // slots, lane s of warp 0 owns slot s in B2 and B3 alike: no barrier in between.
+  const bool b3_warp0 = Lcap <= 32;
+  if (!b3_warp0) __syncthreads();
+  for (int s = b3_warp0 ? (wid == 0 ? lane : Lcap) : tid; s < Lcap; s += b3_warp0 ? 32 : nth) {
     const int o0 = sm.offs[s];
     int o = o0;
     for (int u = 0; u < units; ++u) {
