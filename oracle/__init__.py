@@ -70,6 +70,13 @@ def _load():
         L.orc_filter_cmp.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_int64, _P, _P,
                                      _P, _P, _P]
         L.orc_join_chain_mask.argtypes = [ctypes.c_int, _P, _P, _P, _P, ctypes.c_int64, ctypes.c_uint64, _P, _P, _P]
+        L.orc_pac_hash128_n.argtypes = [_P, ctypes.c_int64, ctypes.c_uint64, _P]
+        L.orc_session_init128.argtypes = [ctypes.c_uint64, _P, _P, _P]
+        L.orc_agg128.restype = ctypes.c_int
+        L.orc_agg128.argtypes = [_P, ctypes.c_int64, _P, _P, ctypes.c_int, _P, ctypes.c_int64, _P, _P,
+                                 ctypes.c_int, _P, _P, _P, _P]
+        L.orc_finalize128.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_int, _P, ctypes.c_int64,
+                                      ctypes.c_int, _P, _P, _P, _P, _P, ctypes.c_uint32, _P, _P, _P, _P]
         L.orc_noised_y.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_int, _P, ctypes.c_int64, _P, _P,
                                    ctypes.c_uint32, _P, _P, _P]
         L.orc_finalize.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_int, _P, ctypes.c_int64,
@@ -338,3 +345,66 @@ def join_chain_mask(tables, fk: np.ndarray, salt: int):
     _load().orc_join_chain_mask(k, pk_p, nx_p, _ptr(nb), _ptr(fk), n, salt & 0xFFFFFFFFFFFFFFFF, _ptr(mask),
                                 _ptr(found), _ptr(pu))
     return mask, found, pu
+
+
+# ------------------------------------------------------------------ m = 128 worlds (§8 f4)
+M128 = 128
+
+
+def pac_hash128(keys: np.ndarray, salt: int) -> np.ndarray:
+    """[n, 2] uint64: (lo = worlds 0..63, hi = worlds 64..127), exactly 64 bits set (R28)."""
+    keys = np.ascontiguousarray(keys, dtype=np.int64)
+    out = np.zeros((len(keys), 2), dtype=np.uint64)
+    _load().orc_pac_hash128_n(_ptr(keys), len(keys), salt & 0xFFFFFFFFFFFFFFFF, _ptr(out))
+    return out
+
+
+def session128(seed: int):
+    js, salt = ctypes.c_int(), ctypes.c_uint64()
+    P = np.zeros(M128, dtype=np.float64)
+    _load().orc_session_init128(seed & 0xFFFFFFFFFFFFFFFF, ctypes.byref(js), ctypes.byref(salt), _ptr(P))
+    return js.value, salt.value, P
+
+
+def agg128(masks: np.ndarray, key_cols, aggs) -> dict:
+    """Grouped 128-world aggregation (R29); masks [n, 2] uint64."""
+    masks = np.ascontiguousarray(masks, dtype=np.uint64).reshape(-1, 2)
+    n = len(masks)
+    nz = np.ascontiguousarray(masks[:, 0] | masks[:, 1])
+    gk = group_keys(key_cols, nz)
+    G = len(gk)
+    kc = _Cols(key_cols)
+    kinds = np.array([k for k, _ in aggs], dtype=np.int32)
+    vals = [None if v is None else np.ascontiguousarray(v) for _, v in aggs]
+    world = []
+    for k, _ in aggs:
+        world.append(None if k == COUNT else np.zeros(G * M128, dtype=np.int64 if k == SUM_I64 else np.float64))
+    vptr = (ctypes.c_void_p * max(1, len(aggs)))(*[None if v is None else v.ctypes.data for v in vals])
+    wptr = (ctypes.c_void_p * max(1, len(aggs)))(*[None if w is None else w.ctypes.data for w in world])
+    rows = np.zeros(G, dtype=np.int64)
+    K = np.zeros(2 * G, dtype=np.uint64)
+    count = np.zeros(G * M128, dtype=np.int64)
+    ovf = _load().orc_agg128(_ptr(masks), n, kc.ptrs, _ptr(kc.eb), kc.n, _ptr(gk), G, _ptr(kinds), vptr, len(aggs),
+                             _ptr(rows), _ptr(K), _ptr(count), wptr)
+    return {"G": G, "keys": gk, "rows": rows, "K": K.reshape(G, 2), "count": count.reshape(G, M128),
+            "world": [None if w is None else w.reshape(G, M128) for w in world],
+            "kinds": [k for k, _ in aggs], "overflow": bool(ovf)}
+
+
+def finalize128(seed: int, B: float, jstar: int, P: np.ndarray, table: dict, round_: int = 0):
+    G = table["G"]
+    A = len(table["kinds"])
+    P = np.array(P, dtype=np.float64, copy=True)
+    kinds = np.array(table["kinds"], dtype=np.int32)
+    world = [None if w is None else np.ascontiguousarray(w) for w in table["world"]]
+    wptr = (ctypes.c_void_p * max(1, A))(*[None if w is None else w.ctypes.data for w in world])
+    release = np.zeros((G, A), dtype=np.float64)
+    is_null = np.zeros((G, A), dtype=np.uint8)
+    flags = np.zeros(G, dtype=np.uint8)
+    delta = np.zeros((G, A), dtype=np.float64)
+    K = np.ascontiguousarray(table["K"], dtype=np.uint64)
+    count = np.ascontiguousarray(table["count"], dtype=np.int64)
+    _load().orc_finalize128(seed & 0xFFFFFFFFFFFFFFFF, float(B), int(jstar), _ptr(P), G, A, _ptr(kinds), _ptr(K),
+                            _ptr(table["rows"]), _ptr(count), wptr, int(round_), _ptr(release), _ptr(is_null),
+                            _ptr(flags), _ptr(delta))
+    return release, is_null, flags, delta, P

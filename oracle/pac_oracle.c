@@ -658,3 +658,213 @@ void orc_join_chain_mask(int k, const int64_t* const* pk, const int64_t* const* 
   }
   for (int t = 0; t < k; t++) free(tab[t]);
 }
+
+/* ------------------------------------------------------------------ m = 128 worlds (§8 f4)
+ * P:L92 (§2, footnote): "Extending to m=128 is possible, and worst-case would double the
+ * cost of our stochastic-aggregates".  Readings R28 (hash), R29 (session, aggregation,
+ * finalize).  A mask is two words: lo = worlds 0..63, hi = worlds 64..127 (R3 extended). */
+#define ORC_M2 128
+
+static int bit128(const uint64_t x[2], int j) { return (int)((x[j >> 6] >> (j & 63)) & 1u); }
+static int popcount128(const uint64_t x[2]) { return popcount64(x[0]) + popcount64(x[1]); }
+
+/* R28: x_lo = fmix64(key XOR salt), x_hi = fmix64(x_lo XOR 0x6A09E667F3BCC909); balance to
+ * exactly 64 ones by the rejection flips of R2 with 7-bit draws: w_0 = fmix64(x_lo XOR x_hi
+ * XOR 0xD1B54A32D192ED03), w_{i+1} = fmix64(w_i + 0x9E3779B97F4A7C15); each word gives 9 draws
+ * p = (w >> 7t) & 127, t = 0..8; a draw flips bit p if it carries the majority value; stop at
+ * k = 0; safety net after 64 words as in R2. */
+void orc_pac_hash128(int64_t key, uint64_t salt, uint64_t out[2]) {
+  uint64_t x[2];
+  x[0] = orc_fmix64((uint64_t)key ^ salt);
+  x[1] = orc_fmix64(x[0] ^ 0x6A09E667F3BCC909ull);
+  int c = popcount128(x);
+  if (c != 64) {
+    int maj = c > 64 ? 1 : 0;
+    int k = c > 64 ? c - 64 : 64 - c;
+    uint64_t w = orc_fmix64(x[0] ^ x[1] ^ 0xD1B54A32D192ED03ull);
+    for (int word = 0; word < 64 && k > 0; word++) {
+      for (int t = 0; t < 9 && k > 0; t++) {
+        int p = (int)((w >> (7 * t)) & 127u);
+        if (bit128(x, p) == maj) {
+          x[p >> 6] ^= 1ull << (p & 63);
+          k--;
+        }
+      }
+      w = orc_fmix64(w + 0x9E3779B97F4A7C15ull);
+    }
+    for (int p = 0; p < ORC_M2 && k > 0; p++) {
+      if (bit128(x, p) == maj) {
+        x[p >> 6] ^= 1ull << (p & 63);
+        k--;
+      }
+    }
+  }
+  out[0] = x[0];
+  out[1] = x[1];
+}
+
+void orc_pac_hash128_n(const int64_t* keys, int64_t n, uint64_t salt, uint64_t* out) {
+  for (int64_t i = 0; i < n; i++) orc_pac_hash128(keys[i], salt, out + 2 * i);
+}
+
+/* R29 session: j* = x0 & 127 of Philox(seed; 0,0,0,TAG_JSTAR), salt as R13, P = 1/128. */
+void orc_session_init128(uint64_t seed, int* jstar, uint64_t* salt, double* P) {
+  uint32_t o[4];
+  philox_block(seed, 0, 0, 0, TAG_JSTAR, o);
+  *jstar = (int)(o[0] & 127u);
+  philox_block(seed, 0, 0, 0, TAG_SALT, o);
+  *salt = (uint64_t)o[0] | ((uint64_t)o[1] << 32);
+  for (int j = 0; j < ORC_M2; j++) P[j] = 1.0 / ORC_M2;
+}
+
+/* R29 aggregation: Eq. counter over 128 worlds; a row is in world j iff bit j of
+ * its 128-bit mask is set; rows with a zero mask are dropped (R21); K[g] = OR of the masks
+ * (two words).  Same output layout as orc_agg_o2 with 128 worlds per group. */
+int orc_agg128(const uint64_t* masks, int64_t n, const void* const* cols, const int32_t* elem_bytes,
+               int n_keys, const uint64_t* gkeys, int64_t G, const int32_t* kinds, const void* const* values,
+               int n_aggs, int64_t* rows, uint64_t* K, int64_t* count, void* const* world) {
+  int overflow = 0;
+  const int64_t GM = G * ORC_M2;
+  for (int64_t g = 0; g < G; g++) { rows[g] = 0; K[2 * g] = K[2 * g + 1] = 0; }
+  for (int64_t i = 0; i < GM; i++) count[i] = 0;
+  for (int a = 0; a < n_aggs; a++) {
+    if (!world[a]) continue;
+    for (int64_t i = 0; i < GM; i++) {
+      if (kinds[a] == K_SUM_I64) ((int64_t*)world[a])[i] = 0;
+      else if (kinds[a] == K_MIN_F64) ((double*)world[a])[i] = INFINITY;
+      else if (kinds[a] == K_MAX_F64) ((double*)world[a])[i] = -INFINITY;
+      else if (kinds[a] != K_COUNT) ((double*)world[a])[i] = 0.0;
+    }
+  }
+  __int128* isum = (__int128*)calloc((size_t)(GM * n_aggs + 1), sizeof(__int128));
+  csum* fsum = (csum*)calloc((size_t)(GM * n_aggs + 1), sizeof(csum));
+  for (int64_t r = 0; r < n; r++) {
+    const uint64_t* h = masks + 2 * r;
+    if ((h[0] | h[1]) == 0) continue;
+    uint64_t key = n_keys ? orc_pack_key(cols, elem_bytes, n_keys, r) : 0;
+    int64_t g = find_group(gkeys, G, key);
+    if (g < 0) continue;
+    rows[g] += 1;
+    K[2 * g] |= h[0];
+    K[2 * g + 1] |= h[1];
+    for (int j = 0; j < ORC_M2; j++) {
+      if (!bit128(h, j)) continue;
+      int64_t cell = g * ORC_M2 + j;
+      count[cell] += 1;
+      for (int a = 0; a < n_aggs; a++) {
+        int64_t idx = (int64_t)a * GM + cell;
+        switch (kinds[a]) {
+          case K_SUM_I64: isum[idx] += (__int128)((const int64_t*)values[a])[r]; break;
+          case K_SUM_F64:
+          case K_AVG_F64: csum_add(&fsum[idx], ((const double*)values[a])[r]); break;
+          case K_MIN_F64: {
+            double v = ((const double*)values[a])[r];
+            double* e = &((double*)world[a])[cell];
+            if (v < *e) *e = v;
+            break;
+          }
+          case K_MAX_F64: {
+            double v = ((const double*)values[a])[r];
+            double* e = &((double*)world[a])[cell];
+            if (v > *e) *e = v;
+            break;
+          }
+          default: break;
+        }
+      }
+    }
+  }
+  for (int a = 0; a < n_aggs; a++) {
+    for (int64_t cell = 0; cell < GM; cell++) {
+      int64_t idx = (int64_t)a * GM + cell;
+      if (kinds[a] == K_SUM_I64) {
+        __int128 v = isum[idx];
+        if (v > (__int128)INT64_MAX || v < (__int128)INT64_MIN) overflow = 1;
+        ((int64_t*)world[a])[cell] = (int64_t)v;
+      } else if (kinds[a] == K_SUM_F64 || kinds[a] == K_AVG_F64) {
+        ((double*)world[a])[cell] = fsum[idx].s + fsum[idx].c;
+      }
+    }
+  }
+  free(isum);
+  free(fsum);
+  return overflow;
+}
+
+static double weighted_var128(const double* P, const double* y) {
+  int first = -1, all_equal = 1;
+  for (int j = 0; j < ORC_M2; j++) {
+    if (P[j] > 0.0) {
+      if (first < 0) first = j;
+      else if (y[j] != y[first]) all_equal = 0;
+    }
+  }
+  if (all_equal) return 0.0;
+  double mu = 0.0;
+  for (int j = 0; j < ORC_M2; j++) mu += P[j] * y[j];
+  double s2 = 0.0;
+  for (int j = 0; j < ORC_M2; j++) s2 += P[j] * (y[j] - mu) * (y[j] - mu);
+  return s2;
+}
+
+static void posterior_update128(double* P, const double* y, double ytilde, double delta) {
+  double d[ORC_M2], dmin = INFINITY;
+  for (int j = 0; j < ORC_M2; j++) {
+    d[j] = (ytilde - y[j]) * (ytilde - y[j]);
+    if (P[j] > 0.0 && d[j] < dmin) dmin = d[j];
+  }
+  double tot = 0.0;
+  for (int j = 0; j < ORC_M2; j++) {
+    if (P[j] > 0.0) P[j] = P[j] * exp(-(d[j] - dmin) / (2.0 * delta));
+    tot += P[j];
+  }
+  for (int j = 0; j < ORC_M2; j++) P[j] = P[j] / tot;
+}
+
+/* R29 finalize: the per-cell steps of orc_finalize over 128 worlds: NULL iff
+ * (x0 >> 25) >= popcount(K) (probability (128 - popcount)/128); y-vectors of R7/R9;
+ * variance and posterior over 128 worlds; diversity flag rows >= 128 and popcount(K) <= 68
+ * (R18 scaled to m = 128). */
+void orc_finalize128(uint64_t seed, double B, int jstar, double* P, int64_t G, int n_aggs, const int32_t* kinds,
+                     const uint64_t* K, const int64_t* rows, const int64_t* count, const void* const* world,
+                     uint32_t round, double* release, uint8_t* is_null, uint8_t* flags, double* delta_out) {
+  double y[ORC_M2];
+  for (int64_t g = 0; g < G; g++) {
+    const uint64_t* Kg = K + 2 * g;
+    int pc = popcount128(Kg);
+    if (flags) flags[g] = (uint8_t)((rows[g] >= 128 && pc <= 68) ? 1 : 0);
+    for (int a = 0; a < n_aggs; a++) {
+      int64_t cell = g * n_aggs + a;
+      uint32_t x[4];
+      philox_block(seed, (uint32_t)cell, (uint32_t)((uint64_t)cell >> 32), round, TAG_CELL, x);
+      if ((int)(x[0] >> 25) >= pc) {
+        is_null[cell] = 1;
+        release[cell] = NAN;
+        if (delta_out) delta_out[cell] = NAN;
+        continue;
+      }
+      is_null[cell] = 0;
+      for (int j = 0; j < ORC_M2; j++) {
+        int64_t c = g * ORC_M2 + j;
+        if (!bit128(Kg, j)) { y[j] = 0.0; continue; }
+        switch (kinds[a]) {
+          case K_COUNT: y[j] = 2.0 * (double)count[c]; break;
+          case K_SUM_I64: y[j] = 2.0 * (double)((const int64_t*)world[a])[c]; break;
+          case K_SUM_F64: y[j] = 2.0 * ((const double*)world[a])[c]; break;
+          case K_AVG_F64: y[j] = ((const double*)world[a])[c] / (double)count[c]; break;
+          default: y[j] = ((const double*)world[a])[c]; break;
+        }
+      }
+      double s2 = weighted_var128(P, y);
+      double delta = s2 / (2.0 * B);
+      if (delta_out) delta_out[cell] = delta;
+      if (s2 == 0.0) {
+        release[cell] = y[jstar];
+        continue;
+      }
+      double yt = y[jstar] + sqrt(delta) * orc_normal(x);
+      release[cell] = yt;
+      posterior_update128(P, y, yt, delta);
+    }
+  }
+}
