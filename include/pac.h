@@ -82,10 +82,17 @@ typedef struct pac_session pac_session;
 /* Creates a session on the current CUDA device.  Errors: PAC_E_INVAL (out NULL,
  * budget_B <= 0 or not finite), PAC_E_CUDA. */
 int pac_session_create(uint64_t seed, double budget_B, pac_session** out);
+/* Session over m = 64 or 128 worlds (§8 f4, R29: j* = x0 & (m-1), P = 1/m; the salt is the
+ * same as for m = 64).  pac_session_create(...) == pac_session_create_m(..., 64, ...).
+ * An m = 128 session finalizes only m = 128 tables; pac_posterior_update / pac_noised_y
+ * are m = 64 only (PAC_E_INVAL otherwise). */
+int pac_session_create_m(uint64_t seed, double budget_B, int32_t m, pac_session** out);
+/* m of the session (0 for NULL). */
+int32_t pac_session_worlds(const pac_session* s);
 /* Frees the session (synchronizes the device).  NULL is a no-op. */
 int pac_session_destroy(pac_session* s);
 /* Synchronizing read of the session state.  Any output pointer may be NULL.
- * h_P64: 64 doubles.  releases: number of non-NULL, non-zero-variance releases so far. */
+ * h_P64: m doubles (64, or 128 for an m = 128 session).  releases: number of non-NULL, non-zero-variance releases so far. */
 int pac_session_query(const pac_session* s, uint64_t* salt, int32_t* jstar, double* h_P64,
                       uint64_t* releases, uint64_t* seed, double* budget_B);
 /* Overwrites the posterior with 64 host doubles (resume / tests).  Synchronizing. */
@@ -126,6 +133,8 @@ typedef struct {
   uint64_t* d_presence;
   int64_t* d_count;
   void* d_world[PAC_MAX_AGGS];
+  int32_t m;  /* worlds per group: 0 or 64, or 128 (§8 f4; then d_presence is [G_cap][2] and
+                 d_count / d_world are [G_cap][128]) */
 } pac_table;
 
 /* Workspace bytes for pac_agg_grouped with these aggregates and capacity. */
@@ -171,8 +180,26 @@ int pac_table_remap(const pac_table* in, const uint64_t* d_union_keys, int64_t G
                     const pac_agg_spec* aggs, int n_aggs, int64_t G_cap_in,
                     const pac_table* out, pac_stream_t stream);
 
+/* ------------------------------------------------------------------ m = 128 worlds (§8 f4)
+ * P:L92 (§2): "Extending to m=128 is possible, and worst-case would double the cost".
+ * Readings R28 (hash), R29 (aggregation, finalize).  A 128-world mask is two words
+ * [n][2] = {lo: worlds 0..63, hi: worlds 64..127}, exactly 64 bits set when hashed. */
+int pac_mask128(const int64_t* d_pu_key, int64_t n, uint64_t salt, uint64_t* d_mask2, pac_stream_t stream);
+/* Workspace bytes of pac_agg_grouped128 (hashing != 0: masks computed from pu keys). */
+int pac_agg_workspace_size128(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, int64_t n_rows, int hashing,
+                              size_t* bytes);
+/* Grouped aggregation over 128 worlds into an m = 128 table (out->m == 128: d_presence
+ * [G_cap][2], d_count and d_world[a] [G_cap][128]).  Same semantics as pac_agg_grouped with
+ * 128 worlds; a row is dropped only when both mask words are 0 (R21).  Implemented as the
+ * 64-world kernels over the two mask halves plus a group/row-count pass, merged on device.
+ * Errors: as pac_agg_grouped. */
+int pac_agg_grouped128(const int64_t* d_pu_key, const uint64_t* d_mask2, uint64_t salt, const pac_key_col* keys,
+                       int n_keys, const pac_agg_spec* aggs, int n_aggs, int64_t n_rows, const pac_table* out,
+                       int64_t G_cap, void* d_ws, size_t ws_bytes, pac_stream_t stream);
+
 /* ------------------------------------------------------------------ finalize (§8 a6-a7)
- * The fused pac_noised step (§2; §4) over every cell of a table,
+ * The fused pac_noised step (§2; §4) over every cell of a table
+ * (m = 64, or m = 128 with an m = 128 session: NULL iff (x0 >> 25) >= popcount(K), R29),
  * cells in canonical order g*n_aggs + a (R12); one call = one round `round`.
  * Per cell (Philox4x32-10 key = session seed, counter = (cell_lo, cell_hi, round, 0)):
  *   NULL iff (x0 >> 26) >= popcount(K[g])                              (R10)

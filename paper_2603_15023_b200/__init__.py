@@ -10,3 +10,4 @@ from .api import (CMP_EQ, CMP_GE, CMP_GT, CMP_LE, CMP_LT, OP_ADD, OP_DIV, OP_MAX
                   OP_SUB, NoisedY, cmp_index, filter_cmp, lift, lift_cmp, noised_y, pac_filter, select,
                   select_cmp, world_vector)
 from .api import JoinTable, join_mask  # noqa: F401
+from .api import Aggregator128, mask128  # noqa: F401

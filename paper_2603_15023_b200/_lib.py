@@ -45,7 +45,7 @@ class Table(ctypes.Structure):
     _fields_ = [("d_num_groups", ctypes.c_void_p), ("d_status", ctypes.c_void_p),
                 ("d_group_key", ctypes.c_void_p), ("d_rows", ctypes.c_void_p),
                 ("d_presence", ctypes.c_void_p), ("d_count", ctypes.c_void_p),
-                ("d_world", ctypes.c_void_p * PAC_MAX_AGGS)]
+                ("d_world", ctypes.c_void_p * PAC_MAX_AGGS), ("m", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -63,6 +63,13 @@ def lib() -> ctypes.CDLL:
     sig = {
         "pac_session_create": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_double, ctypes.POINTER(_P)]),
         "pac_session_destroy": (ctypes.c_int, [_P]),
+        "pac_session_create_m": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_double, ctypes.c_int32, ctypes.POINTER(_P)]),
+        "pac_session_worlds": (ctypes.c_int32, [_P]),
+        "pac_mask128": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_uint64, _P, _P]),
+        "pac_agg_workspace_size128": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                                     _P]),
+        "pac_agg_grouped128": (ctypes.c_int, [_P, _P, ctypes.c_uint64, _P, ctypes.c_int, _P, ctypes.c_int,
+                                              ctypes.c_int64, _P, ctypes.c_int64, _P, ctypes.c_size_t, _P]),
         "pac_session_query": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
         "pac_session_set_posterior": (ctypes.c_int, [_P, _P]),
         "pac_session_posterior_device": (_P, [_P]),
@@ -111,7 +118,8 @@ def check(fn: str, rc: int) -> None:
 
 
 def exported_symbols() -> list:
-    return ["pac_session_create", "pac_session_destroy", "pac_session_query", "pac_session_set_posterior",
+    return ["pac_session_create", "pac_session_create_m", "pac_session_worlds", "pac_mask128",
+            "pac_agg_workspace_size128", "pac_agg_grouped128", "pac_session_destroy", "pac_session_query", "pac_session_set_posterior",
             "pac_session_posterior_device", "pac_mask", "pac_agg_workspace_size", "pac_agg_grouped",
             "pac_table_check", "pac_table_rederive_presence", "pac_table_remap",
             "pac_finalize_workspace_size", "pac_finalize", "pac_posterior_update", "pac_world_vector",

@@ -44,11 +44,12 @@ def _require_cuda(*ts):
 class Session:
     """pac_session: salt, secret world j*, posterior P on the device."""
 
-    def __init__(self, seed: int, budget: float = 1.0 / 128.0):
+    def __init__(self, seed: int, budget: float = 1.0 / 128.0, m: int = PAC_M):
         h = ctypes.c_void_p()
-        check("pac_session_create", L.lib().pac_session_create(seed & 0xFFFFFFFFFFFFFFFF, float(budget),
-                                                                 ctypes.byref(h)))
+        check("pac_session_create_m", L.lib().pac_session_create_m(seed & 0xFFFFFFFFFFFFFFFF, float(budget), int(m),
+                                                                     ctypes.byref(h)))
         self._h = h
+        self.m = int(m)
         self.seed = seed & 0xFFFFFFFFFFFFFFFF
         self.budget = float(budget)
         q = self.query()
@@ -61,7 +62,7 @@ class Session:
     def query(self) -> dict:
         salt, js, rel, seed = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_uint64(), ctypes.c_uint64()
         B = ctypes.c_double()
-        P = np.zeros(PAC_M, dtype=np.float64)
+        P = np.zeros(self.m, dtype=np.float64)
         check("pac_session_query", L.lib().pac_session_query(
             self._h, ctypes.byref(salt), ctypes.byref(js), P.ctypes.data, ctypes.byref(rel),
             ctypes.byref(seed), ctypes.byref(B)))
@@ -112,8 +113,11 @@ class PacTable:
     world: List[Optional[torch.Tensor]]
     _struct: Optional[L.Table] = field(default=None, repr=False)
 
+    m: int = PAC_M
+
     @staticmethod
-    def allocate(kinds: Sequence[int], G_cap: int, device) -> "PacTable":
+    def allocate(kinds: Sequence[int], G_cap: int, device, m: int = PAC_M) -> "PacTable":
+        """m = 64, or 128 (§8 f4: presence [G_cap, 2], count / worlds [G_cap, 128])."""
         kinds = list(kinds)
         mm_only = all(k in (MIN_F64, MAX_F64) for k in kinds)
         z = lambda *s, dt=torch.int64: torch.zeros(*s, dtype=dt, device=device)
@@ -122,11 +126,12 @@ class PacTable:
             if k == COUNT:
                 world.append(None)
             elif k == SUM_I64:
-                world.append(z(G_cap, PAC_M))
+                world.append(z(G_cap, m))
             else:
-                world.append(z(G_cap, PAC_M, dt=torch.float64))
-        return PacTable(kinds, G_cap, z(1), z(1, dt=torch.int32), z(G_cap), z(G_cap), z(G_cap),
-                        None if mm_only else z(G_cap, PAC_M), world)
+                world.append(z(G_cap, m, dt=torch.float64))
+        pres = z(G_cap) if m == PAC_M else z(G_cap, m // 64)
+        return PacTable(kinds, G_cap, z(1), z(1, dt=torch.int32), z(G_cap), z(G_cap), pres,
+                        None if mm_only else z(G_cap, m), world, m=m)
 
     def struct(self) -> L.Table:
         if self._struct is None:
@@ -139,6 +144,7 @@ class PacTable:
             t.d_count = self.count.data_ptr() if self.count is not None else None
             for a, w in enumerate(self.world):
                 t.d_world[a] = w.data_ptr() if w is not None else None
+            t.m = self.m
             self._struct = t
         return self._struct
 
@@ -156,7 +162,7 @@ class PacTable:
             "G": G,
             "keys": as_u64(self.group_key[:G]),
             "rows": self.rows[:G].cpu().numpy(),
-            "K": as_u64(self.presence[:G]),
+            "K": as_u64(self.presence[:G]) if self.m == PAC_M else as_u64(self.presence[:G].contiguous()).reshape(G, -1),
             "count": None if self.count is None else self.count[:G].cpu().numpy(),
             "world": [None if w is None else w[:G].cpu().numpy() for w in self.world],
             "kinds": list(self.kinds),
@@ -221,6 +227,45 @@ class Aggregator:
             _ptr(pu_key), _ptr(mask), salt & 0xFFFFFFFFFFFFFFFF, kc, len(keys), specs, len(aggs), n,
             ctypes.byref(t.struct()), self.G_cap, _ptr(ws), nb, _stream(self.device)))
         return t
+
+
+class Aggregator128:
+    """pac_agg_grouped128 (§8 f4): grouped aggregation over m = 128 worlds (R29)."""
+
+    def __init__(self, kinds: Sequence[int], G_cap: int, device="cuda"):
+        self.kinds = list(kinds)
+        self.G_cap = int(G_cap)
+        self.device = torch.device(device)
+        self.table = PacTable.allocate(self.kinds, self.G_cap, self.device, m=128)
+        self._ws = None
+
+    def __call__(self, values: Sequence[Optional[torch.Tensor]], keys: Sequence[torch.Tensor] = (),
+                 pu_key: Optional[torch.Tensor] = None, mask2: Optional[torch.Tensor] = None,
+                 salt: int = 0) -> PacTable:
+        aggs = list(zip(self.kinds, values))
+        specs = _agg_specs(aggs)
+        kc = _key_cols(keys)
+        _require_cuda(pu_key, mask2)
+        n = pu_key.numel() if pu_key is not None else mask2.shape[0]
+        nb = ctypes.c_size_t()
+        check("pac_agg_workspace_size128", L.lib().pac_agg_workspace_size128(
+            specs, len(aggs), self.G_cap, n, 1 if pu_key is not None else 0, ctypes.byref(nb)))
+        if self._ws is None or self._ws.numel() < nb.value:
+            self._ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=self.device)
+        t = self.table
+        check("pac_agg_grouped128", L.lib().pac_agg_grouped128(
+            _ptr(pu_key), _ptr(mask2), salt & 0xFFFFFFFFFFFFFFFF, kc, len(keys), specs, len(aggs), n,
+            ctypes.byref(t.struct()), self.G_cap, _ptr(self._ws), nb.value, _stream(self.device)))
+        return t
+
+
+def mask128(pu_keys: torch.Tensor, salt: int) -> torch.Tensor:
+    """pac_hash over 128 worlds (R28): int64 [n, 2] bit patterns (lo, hi)."""
+    _require_cuda(pu_keys)
+    out = torch.empty(pu_keys.numel(), 2, dtype=torch.int64, device=pu_keys.device)
+    check("pac_mask128", L.lib().pac_mask128(_ptr(pu_keys), pu_keys.numel(), salt & 0xFFFFFFFFFFFFFFFF, _ptr(out),
+                                              _stream(pu_keys.device)))
+    return out
 
 
 def agg_grouped(aggs: Sequence[Tuple[int, Optional[torch.Tensor]]], keys: Sequence[torch.Tensor] = (),

@@ -747,7 +747,7 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
                                const pac_key_col* keys, int n_keys, const pac_agg_spec* aggs, int n_aggs,
                                int64_t n_rows, const pac_table* out, int64_t G_cap, void* d_ws,
                                size_t ws_bytes, pac_stream_t stream) {
-  if (n_rows < 0 || !out || G_cap < 1) return PAC_E_INVAL;
+  if (n_rows < 0 || !out || G_cap < 1 || (out->m != 0 && out->m != 64)) return PAC_E_INVAL;  // m = 128: pac_agg_grouped128
   // exactly one mask source (an empty input may arrive as NULL pointers)
   if (d_pu_key && d_mask) return PAC_E_INVAL;
   if (!d_pu_key && !d_mask && n_rows > 0) return PAC_E_INVAL;
@@ -1002,7 +1002,7 @@ __global__ void k_remap(pac_table in, const uint64_t* ukeys, int64_t Gu, pac_tab
 extern "C" int pac_table_rederive_presence(const pac_table* t, const pac_agg_spec* aggs, int n_aggs,
                                            int64_t G_cap, pac_stream_t stream) {
   AccSet A;
-  if (!t || G_cap < 1) return PAC_E_INVAL;
+  if (!t || G_cap < 1 || (t->m != 0 && t->m != 64)) return PAC_E_INVAL;  // m = 64 tables
   int rc = build_accs(aggs, n_aggs, &A, true, true);  // only the kinds matter here
   if (rc) return rc;
   int mm_a = -1, mm_kind = 0;
@@ -1024,6 +1024,7 @@ extern "C" int pac_table_remap(const pac_table* in, const uint64_t* d_union_keys
                                pac_stream_t stream) {
   AccSet A;
   if (!in || !out || !d_union_keys || G_union < 1 || G_cap_in < 1) return PAC_E_INVAL;
+  if ((in->m != 0 && in->m != 64) || (out->m != 0 && out->m != 64)) return PAC_E_INVAL;  // m = 64 tables
   int rc = build_accs(aggs, n_aggs, &A, true, true);  // only the kinds matter here
   if (rc) return rc;
   // kinds are passed by value through a small device buffer embedded in the launch

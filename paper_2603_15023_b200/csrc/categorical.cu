@@ -230,7 +230,8 @@ static int launched() {
 
 extern "C" int pac_world_vector(const pac_table* t, const pac_agg_spec* aggs, int n_aggs, int a, int64_t G_cap,
                                 double* d_y, uint64_t* d_presence, pac_stream_t stream) {
-  if (!t || !aggs || a < 0 || a >= n_aggs || n_aggs > PAC_MAX_AGGS || G_cap < 1 || !d_y || !d_presence)
+  if (!t || !aggs || a < 0 || a >= n_aggs || n_aggs > PAC_MAX_AGGS || G_cap < 1 || !d_y || !d_presence ||
+      (t->m != 0 && t->m != 64))  // world vectors are m = 64 (R22)
     return PAC_E_INVAL;
   const int kind = aggs[a].kind;
   if (kind < PAC_COUNT || kind > PAC_MAX_F64 || !t->d_num_groups || !t->d_presence) return PAC_E_INVAL;

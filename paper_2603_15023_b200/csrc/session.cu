@@ -15,14 +15,15 @@ struct pac_session {
   double B;
   int32_t jstar;
   uint64_t salt;
-  double* d_P;                  // [64]
+  double* d_P;                  // [m]
   unsigned long long* d_count;  // releases counter
+  int32_t m;                    // worlds: 64, or 128 (§8 f4, R29)
 };
 
 namespace pac {
 
-__global__ void k_session_init(double* P, unsigned long long* cnt) {
-  if (threadIdx.x < kM) P[threadIdx.x] = 1.0 / kM;
+__global__ void k_session_init(double* P, unsigned long long* cnt, int m) {
+  if (threadIdx.x < m) P[threadIdx.x] = 1.0 / m;
   if (threadIdx.x == 0) *cnt = 0;
 }
 
@@ -57,18 +58,20 @@ struct FinPrep {
   int kinds[PAC_MAX_AGGS];
   const void* world[PAC_MAX_AGGS];
   const int64_t* count;
-  const uint64_t* K;
+  const uint64_t* K;  // [G][M/64] words
   const int64_t* rows;
   uint64_t seed;
   uint32_t round;
-  double* ybuf;     // [cells][64]
+  double* ybuf;     // [cells][M]
   double* zbuf;     // [cells]
   uint8_t* is_null; // [cells]
   uint8_t* flags;   // [G]
 };
 
-// one warp per cell
+// one warp per cell; M = 64 or 128 worlds (lane owns worlds lane + 32h, h < M/32)
+template <int M>
 __global__ void k_finalize_prep(FinPrep f) {
+  constexpr int W = M / 64;
   const int64_t G = min(*f.num_groups, f.G_cap);
   const int64_t cells = G * f.A;
   const int lane = threadIdx.x & 31;
@@ -77,17 +80,19 @@ __global__ void k_finalize_prep(FinPrep f) {
        cell += (int64_t)gridDim.x * wpb) {
     const int64_t g = cell / f.A;
     const int a = (int)(cell % f.A);
-    const uint64_t Kg = f.K[g];
-    const int pc = __popcll(Kg);
+    int pc = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) pc += __popcll(f.K[g * W + w]);
     const u32x4 x = philox4x32_10({(uint32_t)cell, (uint32_t)((uint64_t)cell >> 32), f.round, kTagCell},
                                   (uint32_t)f.seed, (uint32_t)(f.seed >> 32));
-    const bool null = (int)(x.x >> 26) >= pc;  // R10
+    const bool null = (int)(x.x >> (M == 64 ? 26 : 25)) >= pc;  // R10 / R29
     const int kind = f.kinds[a];
-    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int h = 0; h < M / 32; ++h) {
       const int j = lane + 32 * h;
-      const size_t c = (size_t)g * kM + j;
+      const size_t c = (size_t)g * M + j;
       double y = 0.0;
-      if ((Kg >> j) & 1ull) {  // R9: unset worlds read 0
+      if ((f.K[g * W + (j >> 6)] >> (j & 63)) & 1ull) {  // R9: unset worlds read 0
         switch (kind) {
           case PAC_COUNT: y = 2.0 * (double)f.count[c]; break;
           case PAC_SUM_I64: y = 2.0 * (double)((const int64_t*)f.world[a])[c]; break;
@@ -96,12 +101,12 @@ __global__ void k_finalize_prep(FinPrep f) {
           default: y = ((const double*)f.world[a])[c]; break;
         }
       }
-      f.ybuf[cell * kM + j] = y;
+      f.ybuf[cell * M + j] = y;
     }
     if (lane == 0) {
       f.is_null[cell] = null ? 1 : 0;
       f.zbuf[cell] = null ? 0.0 : normal_from(x);
-      if (a == 0 && f.flags) f.flags[g] = (f.rows[g] >= 64 && pc <= 34) ? 1 : 0;  // R18
+      if (a == 0 && f.flags) f.flags[g] = (f.rows[g] >= M && pc <= (M == 64 ? 34 : 68)) ? 1 : 0;  // R18 / R29
     }
   }
 }
@@ -129,45 +134,56 @@ __global__ void k_noised_prep_y(const double* __restrict__ y, const uint64_t* __
   }
 }
 
-// P <- P*W / sum(P*W) over worlds with P_j > 0 (R14); lane owns j, j+32
-__device__ __forceinline__ void bayes_update(double& p0, double& p1, double y0, double y1, double yt,
-                                             double delta) {
-  const double d0 = __dmul_rn(__dsub_rn(yt, y0), __dsub_rn(yt, y0));
-  const double d1 = __dmul_rn(__dsub_rn(yt, y1), __dsub_rn(yt, y1));
-  const double dmin = warp_min(fmin(p0 > 0.0 ? d0 : INFINITY, p1 > 0.0 ? d1 : INFINITY));
+// P <- P*W / sum(P*W) over worlds with P_j > 0 (R14); lane owns worlds lane + 32h
+template <int H>
+__device__ __forceinline__ void bayes_update(double (&p)[H], const double (&y)[H], double yt, double delta) {
+  double d[H];
+  double lmin = INFINITY;
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    d[h] = __dmul_rn(__dsub_rn(yt, y[h]), __dsub_rn(yt, y[h]));
+    lmin = fmin(lmin, p[h] > 0.0 ? d[h] : INFINITY);
+  }
+  const double dmin = warp_min(lmin);
   const double two_delta = 2.0 * delta;
-  if (p0 > 0.0) p0 = __dmul_rn(p0, exp(-__ddiv_rn(__dsub_rn(d0, dmin), two_delta)));
-  if (p1 > 0.0) p1 = __dmul_rn(p1, exp(-__ddiv_rn(__dsub_rn(d1, dmin), two_delta)));
-  const double tot = warp_sum(p0 + p1);
-  p0 = __ddiv_rn(p0, tot);
-  p1 = __ddiv_rn(p1, tot);
+  double lsum = 0.0;
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    if (p[h] > 0.0) p[h] = __dmul_rn(p[h], exp(-__ddiv_rn(__dsub_rn(d[h], dmin), two_delta)));
+    lsum += p[h];
+  }
+  const double tot = warp_sum(lsum);
+#pragma unroll
+  for (int h = 0; h < H; ++h) p[h] = __ddiv_rn(p[h], tot);
 }
 
-// one warp: the sequential release chain
+// one warp: the sequential release chain over M worlds (H = M/32 per lane)
 // num_groups == nullptr: G_cap cells-per-aggregate rows are all valid (pac_noised_y)
+template <int M>
 __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups, int64_t G_cap, int A,
                                                        const double* __restrict__ ybuf,
                                                        const double* __restrict__ zbuf,
                                                        const uint8_t* __restrict__ is_null, double* P,
                                                        unsigned long long* releases, int jstar, double B,
                                                        double* release, double* delta_out) {
+  constexpr int H = M / 32;
   const int lane = threadIdx.x;
   const int64_t G = num_groups ? min(*num_groups, G_cap) : G_cap;
   const int64_t cells = G * A;
-  double p0 = P[lane], p1 = P[lane + 32];
-  unsigned long long nrel = 0;
-  const int jl = jstar & 31;
-  const bool jhi = jstar >= 32;
-  double ny0 = 0, ny1 = 0;
-  if (cells > 0) {
-    ny0 = ybuf[lane];
-    ny1 = ybuf[lane + 32];
+  double p[H], ny[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    p[h] = P[lane + 32 * h];
+    ny[h] = cells > 0 ? ybuf[lane + 32 * h] : 0.0;
   }
+  unsigned long long nrel = 0;
+  const int jl = jstar & 31, jh = jstar >> 5;
   for (int64_t cell = 0; cell < cells; ++cell) {
-    const double y0 = ny0, y1 = ny1;
-    if (cell + 1 < cells) {  // prefetch the next cell's y-vector
-      ny0 = ybuf[(cell + 1) * kM + lane];
-      ny1 = ybuf[(cell + 1) * kM + lane + 32];
+    double y[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      y[h] = ny[h];
+      if (cell + 1 < cells) ny[h] = ybuf[(cell + 1) * M + lane + 32 * h];  // prefetch the next cell
     }
     if (is_null[cell]) {
       if (lane == 0) {
@@ -177,9 +193,16 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
       continue;
     }
     // R11: zero variance iff every y_j with P_j > 0 is equal
-    const double lo = warp_min(fmin(p0 > 0.0 ? y0 : INFINITY, p1 > 0.0 ? y1 : INFINITY));
-    const double hi = warp_max(fmax(p0 > 0.0 ? y0 : -INFINITY, p1 > 0.0 ? y1 : -INFINITY));
-    const double yj = __shfl_sync(0xffffffffu, jhi ? y1 : y0, jl);
+    double llo = INFINITY, lhi = -INFINITY, lmu = 0.0, yjl = 0.0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      llo = fmin(llo, p[h] > 0.0 ? y[h] : INFINITY);
+      lhi = fmax(lhi, p[h] > 0.0 ? y[h] : -INFINITY);
+      lmu += __dmul_rn(p[h], y[h]);
+      if (h == jh) yjl = y[h];
+    }
+    const double lo = warp_min(llo), hi = warp_max(lhi);
+    const double yj = __shfl_sync(0xffffffffu, yjl, jl);
     if (lo == hi) {
       if (lane == 0) {
         release[cell] = yj;
@@ -188,9 +211,14 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
       continue;
     }
     // R8: population variance under P, two-pass
-    const double mu = warp_sum(__dmul_rn(p0, y0) + __dmul_rn(p1, y1));
-    const double e0 = __dsub_rn(y0, mu), e1 = __dsub_rn(y1, mu);
-    const double s2 = warp_sum(__dmul_rn(__dmul_rn(p0, e0), e0) + __dmul_rn(__dmul_rn(p1, e1), e1));
+    const double mu = warp_sum(lmu);
+    double ls2 = 0.0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const double e = __dsub_rn(y[h], mu);
+      ls2 += __dmul_rn(__dmul_rn(p[h], e), e);
+    }
+    const double s2 = warp_sum(ls2);
     const double delta = __ddiv_rn(s2, 2.0 * B);
     if (s2 == 0.0) {  // all weight on worlds equal up to rounding
       if (lane == 0) {
@@ -200,29 +228,30 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
       continue;
     }
     const double yt = __dadd_rn(yj, __dmul_rn(sqrt(delta), zbuf[cell]));
-    bayes_update(p0, p1, y0, y1, yt, delta);
+    bayes_update<H>(p, y, yt, delta);
     ++nrel;
     if (lane == 0) {
       release[cell] = yt;
       if (delta_out) delta_out[cell] = delta;
     }
   }
-  P[lane] = p0;
-  P[lane + 32] = p1;
+#pragma unroll
+  for (int h = 0; h < H; ++h) P[lane + 32 * h] = p[h];
   if (lane == 0) *releases += nrel;
 }
 
 __global__ void __launch_bounds__(32) k_posterior_update(double* P, const double* y, double yt, double delta) {
   const int lane = threadIdx.x;
-  double p0 = P[lane], p1 = P[lane + 32];
-  bayes_update(p0, p1, y[lane], y[lane + 32], yt, delta);
-  P[lane] = p0;
-  P[lane + 32] = p1;
+  double p[2] = {P[lane], P[lane + 32]};
+  const double yy[2] = {y[lane], y[lane + 32]};
+  bayes_update<2>(p, yy, yt, delta);
+  P[lane] = p[0];
+  P[lane + 32] = p[1];
 }
 
-static size_t fin_ws(int64_t G_cap, int A, size_t* o_z, size_t* o_n) {
+static size_t fin_ws(int64_t G_cap, int A, size_t* o_z, size_t* o_n, int M = kM) {
   const size_t cells = (size_t)G_cap * A;
-  size_t y = cells * kM * 8;
+  size_t y = cells * M * 8;
   *o_z = (y + 255) & ~(size_t)255;
   size_t z = cells * 8;
   *o_n = (*o_z + z + 255) & ~(size_t)255;
@@ -235,28 +264,35 @@ uint64_t session_seed(const pac_session* s) { return s->seed; }
 
 using namespace pac;
 
-extern "C" int pac_session_create(uint64_t seed, double budget_B, pac_session** out) {
-  if (!out || !(budget_B > 0.0) || !std::isfinite(budget_B)) return PAC_E_INVAL;
+extern "C" int pac_session_create_m(uint64_t seed, double budget_B, int32_t m, pac_session** out) {
+  if (!out || !(budget_B > 0.0) || !std::isfinite(budget_B) || (m != 64 && m != 128)) return PAC_E_INVAL;
   pac_session* s = new (std::nothrow) pac_session();
   if (!s) return PAC_E_INVAL;
   s->seed = seed;
   s->B = budget_B;
-  // R13: j* and salt from Philox(seed; 0,0,0,tag)
+  s->m = m;
+  // R13 / R29: j* and salt from Philox(seed; 0,0,0,tag)
   u32x4 a = philox4x32_10({0, 0, 0, kTagJstar}, (uint32_t)seed, (uint32_t)(seed >> 32));
-  s->jstar = (int32_t)(a.x & 63u);
+  s->jstar = (int32_t)(a.x & (uint32_t)(m - 1));
   u32x4 b = philox4x32_10({0, 0, 0, kTagSalt}, (uint32_t)seed, (uint32_t)(seed >> 32));
   s->salt = (uint64_t)b.x | ((uint64_t)b.y << 32);
-  if (cudaMalloc(&s->d_P, kM * sizeof(double)) != cudaSuccess ||
+  if (cudaMalloc(&s->d_P, m * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&s->d_count, sizeof(unsigned long long)) != cudaSuccess) {
     delete s;
     return PAC_E_CUDA;
   }
-  k_session_init<<<1, 64>>>(s->d_P, s->d_count);
+  k_session_init<<<1, 128>>>(s->d_P, s->d_count, m);
   note_launch();
   if (cudaDeviceSynchronize() != cudaSuccess) return PAC_E_CUDA;
   *out = s;
   return PAC_OK;
 }
+
+extern "C" int pac_session_create(uint64_t seed, double budget_B, pac_session** out) {
+  return pac_session_create_m(seed, budget_B, 64, out);
+}
+
+extern "C" int32_t pac_session_worlds(const pac_session* s) { return s ? s->m : 0; }
 
 extern "C" int pac_session_destroy(pac_session* s) {
   if (!s) return PAC_OK;
@@ -275,7 +311,7 @@ extern "C" int pac_session_query(const pac_session* s, uint64_t* salt, int32_t* 
   if (jstar) *jstar = s->jstar;
   if (seed) *seed = s->seed;
   if (budget_B) *budget_B = s->B;
-  if (h_P64 && cudaMemcpy(h_P64, s->d_P, kM * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return PAC_E_CUDA;
+  if (h_P64 && cudaMemcpy(h_P64, s->d_P, s->m * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return PAC_E_CUDA;
   if (releases) {
     unsigned long long c = 0;
     if (cudaMemcpy(&c, s->d_count, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return PAC_E_CUDA;
@@ -286,7 +322,7 @@ extern "C" int pac_session_query(const pac_session* s, uint64_t* salt, int32_t* 
 
 extern "C" int pac_session_set_posterior(pac_session* s, const double* h_P64) {
   if (!s || !h_P64) return PAC_E_INVAL;
-  if (cudaMemcpy(s->d_P, h_P64, kM * 8, cudaMemcpyHostToDevice) != cudaSuccess) return PAC_E_CUDA;
+  if (cudaMemcpy(s->d_P, h_P64, s->m * 8, cudaMemcpyHostToDevice) != cudaSuccess) return PAC_E_CUDA;
   return cudaDeviceSynchronize() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
 
@@ -295,7 +331,7 @@ extern "C" double* pac_session_posterior_device(pac_session* s) { return s ? s->
 extern "C" int pac_finalize_workspace_size(int64_t G_cap, int n_aggs, size_t* bytes) {
   if (!bytes || G_cap < 1 || n_aggs < 1 || n_aggs > PAC_MAX_AGGS) return PAC_E_INVAL;
   size_t oz, on;
-  *bytes = fin_ws(G_cap, n_aggs, &oz, &on);
+  *bytes = fin_ws(G_cap, n_aggs, &oz, &on, 128);  // enough for m = 64 and m = 128 tables
   return PAC_OK;
 }
 
@@ -314,8 +350,10 @@ extern "C" int pac_finalize(pac_session* s, const pac_table* t, const pac_agg_sp
     if (k != PAC_COUNT && !t->d_world[a]) return PAC_E_INVAL;
   }
   if (need_count && !t->d_count) return PAC_E_INVAL;
+  const int M = t->m ? t->m : 64;
+  if (M != s->m) return PAC_E_INVAL;  // the table and the session must agree on m (R29)
   size_t oz, on;
-  const size_t need = fin_ws(G_cap, n_aggs, &oz, &on);
+  const size_t need = fin_ws(G_cap, n_aggs, &oz, &on, M);
   if (!d_ws || ws_bytes < need) return PAC_E_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)d_ws;
@@ -338,17 +376,25 @@ extern "C" int pac_finalize(pac_session* s, const pac_table* t, const pac_agg_sp
   f.flags = d_flags;
   const int64_t cells = G_cap * n_aggs;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((cells + 7) / 8, 148 * 32));
-  k_finalize_prep<<<blocks, 256, 0, st>>>(f);
-  note_launch();
-  k_finalize_chain<<<1, 32, 0, st>>>(t->d_num_groups, G_cap, n_aggs, f.ybuf, f.zbuf, d_is_null, s->d_P,
-                                     s->d_count, s->jstar, s->B, d_release, d_delta);
+  if (M == 64) {
+    k_finalize_prep<64><<<blocks, 256, 0, st>>>(f);
+    note_launch();
+    k_finalize_chain<64><<<1, 32, 0, st>>>(t->d_num_groups, G_cap, n_aggs, f.ybuf, f.zbuf, d_is_null, s->d_P,
+                                           s->d_count, s->jstar, s->B, d_release, d_delta);
+  } else {
+    k_finalize_prep<128><<<blocks, 256, 0, st>>>(f);
+    note_launch();
+    k_finalize_chain<128><<<1, 32, 0, st>>>(t->d_num_groups, G_cap, n_aggs, f.ybuf, f.zbuf, d_is_null, s->d_P,
+                                            s->d_count, s->jstar, s->B, d_release, d_delta);
+  }
   note_launch();
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
 
 extern "C" int pac_posterior_update(pac_session* s, const double* d_y64, double y_tilde, double delta,
                                     pac_stream_t stream) {
-  if (!s || !d_y64 || !(delta > 0.0) || !std::isfinite(delta) || !std::isfinite(y_tilde)) return PAC_E_INVAL;
+  if (!s || !d_y64 || !(delta > 0.0) || !std::isfinite(delta) || !std::isfinite(y_tilde) || s->m != 64)
+    return PAC_E_INVAL;
   k_posterior_update<<<1, 32, 0, (cudaStream_t)stream>>>(s->d_P, d_y64, y_tilde, delta);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
@@ -364,7 +410,8 @@ extern "C" int pac_noised_y_workspace_size(int64_t n, size_t* bytes) {
 extern "C" int pac_noised_y(pac_session* s, const double* d_y, const uint64_t* d_presence, int64_t n, uint32_t round,
                             double* d_release, uint8_t* d_is_null, double* d_delta, void* d_ws, size_t ws_bytes,
                             pac_stream_t stream) {
-  if (!s || n < 0 || (n > 0 && (!d_y || !d_presence || !d_release || !d_is_null))) return PAC_E_INVAL;
+  if (!s || s->m != 64 || n < 0 || (n > 0 && (!d_y || !d_presence || !d_release || !d_is_null)))
+    return PAC_E_INVAL;
   if (n == 0) return PAC_OK;
   size_t oz, on;
   const size_t need = fin_ws(n, 1, &oz, &on);
@@ -376,8 +423,8 @@ extern "C" int pac_noised_y(pac_session* s, const double* d_y, const uint64_t* d
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, 148 * 32));
   k_noised_prep_y<<<blocks, 256, 0, st>>>(d_y, d_presence, n, s->seed, round, ybuf, zbuf, d_is_null);
   note_launch();
-  k_finalize_chain<<<1, 32, 0, st>>>(nullptr, n, 1, ybuf, zbuf, d_is_null, s->d_P, s->d_count, s->jstar, s->B,
-                                     d_release, d_delta);
+  k_finalize_chain<64><<<1, 32, 0, st>>>(nullptr, n, 1, ybuf, zbuf, d_is_null, s->d_P, s->d_count, s->jstar,
+                                         s->B, d_release, d_delta);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
