@@ -43,6 +43,25 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+constexpr int kChainChunk = 16;  // cells per staged chunk of k_finalize_chain
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc)
+               : "memory");
+}
+// 16-byte async copy of `bytes` (<= 16) source bytes, the rest of the 16 zero-filled
+__device__ __forceinline__ void cp_async16z(void* smem_dst, const void* gsrc, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Box-Muller normal from one Philox block (R13).
 __device__ __forceinline__ double normal_from(u32x4 x) {
   const uint64_t m53 = ((uint64_t)x.y << 21) ^ (uint64_t)(x.z >> 11);
@@ -157,7 +176,17 @@ __device__ __forceinline__ void bayes_update(double (&p)[H], const double (&y)[H
   for (int h = 0; h < H; ++h) p[h] = __ddiv_rn(p[h], tot);
 }
 
-// one warp: the sequential release chain over M worlds (H = M/32 per lane)
+// one warp: the sequential release chain over M worlds (H = M/32 per lane).
+// Latency-bound (each cell's variance is taken under the posterior the previous cell left), so
+// the chain keeps two dependent warp reductions per released cell:
+//   pass 1: sum P, sum P*y, min and max of y over P > 0 (four independent trees)
+//   pass 2: sum P*(y - mu)^2
+// and no reduction in the update: the posterior is normalised at the next released cell with the
+// mass pass 1 sums anyway (and when the chain ends), and the likelihood
+// is shifted by d_{j*} = (y~ - y_{j*})^2 = Delta*z^2 instead of min_j d_j -- both shifts cancel
+// in the normalisation (R14), and W_j = exp((d_{j*} - d_j)/(2 Delta)) <= exp(z^2/2) cannot
+// overflow while W_{j*} = 1 keeps the weights from vanishing together.  Equal to the oracle's
+// per-cell normalised update up to rounding (R16).
 // num_groups == nullptr: G_cap cells-per-aggregate rows are all valid (pac_noised_y)
 template <int M>
 __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups, int64_t G_cap, int A,
@@ -167,51 +196,91 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
                                                        unsigned long long* releases, int jstar, double B,
                                                        double* release, double* delta_out) {
   constexpr int H = M / 32;
+  constexpr int CH = kChainChunk;
+  // cells are streamed through shared memory in chunks of CH (double-buffered cp.async), so
+  // the chain never waits on HBM latency: y-vectors, normals and NULL flags of chunk c+1 are in
+  // flight while chunk c is released
+  __shared__ __align__(16) double sy[2][CH * M];
+  __shared__ __align__(16) double sz[2][CH];
+  __shared__ __align__(16) uint8_t sn[2][CH];
   const int lane = threadIdx.x;
   const int64_t G = num_groups ? min(*num_groups, G_cap) : G_cap;
   const int64_t cells = G * A;
-  double p[H], ny[H];
+  const int64_t nchunks = (cells + CH - 1) / CH;
+  auto stage = [&](int64_t c) {
+    const int b = (int)(c & 1);
+    const int64_t c0 = c * CH;
+    const int nc = (int)min((int64_t)CH, cells - c0);
+    const char* gy = (const char*)(ybuf + c0 * M);
+    char* dy = (char*)sy[b];
+    for (int i = lane; i < nc * M / 2; i += 32) cp_async16(dy + 16 * i, gy + 16 * i);
+    // normals: nc doubles in 16-byte pieces; NULL flags: nc bytes in one piece (zero-filled tails)
+    if (lane < (nc + 1) / 2) {
+      const int bytes = min(16, 8 * (nc - 2 * lane));
+      cp_async16z((char*)sz[b] + 16 * lane, (const char*)(zbuf + c0) + 16 * lane, bytes);
+    }
+    if (lane == 31) cp_async16z(sn[b], is_null + c0, nc);
+    cp_async_commit();
+  };
+  double p[H];
 #pragma unroll
-  for (int h = 0; h < H; ++h) {
-    p[h] = P[lane + 32 * h];
-    ny[h] = cells > 0 ? ybuf[lane + 32 * h] : 0.0;
-  }
+  for (int h = 0; h < H; ++h) p[h] = P[lane + 32 * h];
   unsigned long long nrel = 0;
   const int jl = jstar & 31, jh = jstar >> 5;
+  if (nchunks > 0) stage(0);
   for (int64_t cell = 0; cell < cells; ++cell) {
+    const int ci = (int)(cell % CH);
+    const int b = (int)((cell / CH) & 1);
+    if (ci == 0) {
+      __syncwarp();  // every lane is done with the buffer chunk c+1 overwrites
+      if (cell / CH + 1 < nchunks) {
+        stage(cell / CH + 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+    }
     double y[H];
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
-      y[h] = ny[h];
-      if (cell + 1 < cells) ny[h] = ybuf[(cell + 1) * M + lane + 32 * h];  // prefetch the next cell
-    }
-    if (is_null[cell]) {
+    for (int h = 0; h < H; ++h) y[h] = sy[b][ci * M + lane + 32 * h];
+    if (sn[b][ci]) {
       if (lane == 0) {
         release[cell] = NAN;
         if (delta_out) delta_out[cell] = NAN;
       }
       continue;
     }
-    // R11: zero variance iff every y_j with P_j > 0 is equal
-    double llo = INFINITY, lhi = -INFINITY, lmu = 0.0, yjl = 0.0;
+    // pass 1: R11 zero-variance test, the P-mass and the P-weighted sum
+    double llo = INFINITY, lhi = -INFINITY, lsp = 0.0, lspy = 0.0, yjl = 0.0;
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       llo = fmin(llo, p[h] > 0.0 ? y[h] : INFINITY);
       lhi = fmax(lhi, p[h] > 0.0 ? y[h] : -INFINITY);
-      lmu += __dmul_rn(p[h], y[h]);
+      lsp += p[h];
+      lspy += __dmul_rn(p[h], y[h]);
       if (h == jh) yjl = y[h];
     }
-    const double lo = warp_min(llo), hi = warp_max(lhi);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      llo = fmin(llo, __shfl_xor_sync(0xffffffffu, llo, d));
+      lhi = fmax(lhi, __shfl_xor_sync(0xffffffffu, lhi, d));
+      lsp += __shfl_xor_sync(0xffffffffu, lsp, d);
+      lspy += __shfl_xor_sync(0xffffffffu, lspy, d);
+    }
     const double yj = __shfl_sync(0xffffffffu, yjl, jl);
-    if (lo == hi) {
+    if (llo == lhi) {
       if (lane == 0) {
         release[cell] = yj;
         if (delta_out) delta_out[cell] = 0.0;
       }
       continue;
     }
-    // R8: population variance under P, two-pass
-    const double mu = warp_sum(lmu);
+    // the previous update's normalisation, with the mass pass 1 just summed (no extra reduction)
+#pragma unroll
+    for (int h = 0; h < H; ++h) p[h] = __ddiv_rn(p[h], lsp);
+    // pass 2: R8 population variance under P, two-pass
+    const double mu = __ddiv_rn(lspy, lsp);
     double ls2 = 0.0;
 #pragma unroll
     for (int h = 0; h < H; ++h) {
@@ -227,16 +296,30 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
       }
       continue;
     }
-    const double yt = __dadd_rn(yj, __dmul_rn(sqrt(delta), zbuf[cell]));
-    bayes_update<H>(p, y, yt, delta);
+    const double z = sz[b][ci];
+    const double yt = __dadd_rn(yj, __dmul_rn(sqrt(delta), z));
+    // Bayesian update, shifted by d_{j*} (see above), no normalisation
+    const double dj = __dmul_rn(__dsub_rn(yt, yj), __dsub_rn(yt, yj));
+    const double inv2d = __drcp_rn(2.0 * delta);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const double d = __dmul_rn(__dsub_rn(yt, y[h]), __dsub_rn(yt, y[h]));
+      if (p[h] > 0.0) p[h] = __dmul_rn(p[h], exp(__dmul_rn(__dsub_rn(dj, d), inv2d)));
+    }
     ++nrel;
     if (lane == 0) {
       release[cell] = yt;
       if (delta_out) delta_out[cell] = delta;
     }
   }
+  const double tot = warp_sum([&] {
+    double t = 0.0;
 #pragma unroll
-  for (int h = 0; h < H; ++h) P[lane + 32 * h] = p[h];
+    for (int h = 0; h < H; ++h) t += p[h];
+    return t;
+  }());
+#pragma unroll
+  for (int h = 0; h < H; ++h) P[lane + 32 * h] = __ddiv_rn(p[h], tot);
   if (lane == 0) *releases += nrel;
 }
 
