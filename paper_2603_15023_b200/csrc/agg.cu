@@ -20,6 +20,7 @@
 
 #include "agg_tiles.cuh"
 #include "agg_warp.cuh"
+#include "agg_tm.cuh"
 
 namespace pac {
 
@@ -460,8 +461,10 @@ static int raw_tile_bytes(const AccSet& A, int T, int key_bytes) {
   return cols8 * T * 8 + ((key_bytes * T + 15) & ~15) + 16 * PAC_MAX_KEYS;
 }
 
-static SmemLayout make_layout(const AccSet& A, int T, int Lcap, int key_bytes = 8) {
+static SmemLayout make_layout(const AccSet& A, int T, int Lcap, int key_bytes = 8, bool tm = false) {
   SmemLayout L{};
+  L.tm = tm ? 1 : 0;
+  const int tl = tm ? 0 : Lcap;  // slots of the smem CTA table (none in TMEM mode)
   L.T = T;
   L.TS = T + 8 * Lcap;  // slot-sorted staging, each slot padded to a multiple of 8 rows
   L.Lcap = Lcap;
@@ -474,10 +477,10 @@ static SmemLayout make_layout(const AccSet& A, int T, int Lcap, int key_bytes = 
   };
   const bool mm = A.has_min || A.has_max;
   const int TS = L.TS;
-  L.o_isum = take(A.ni * Lcap * kM * 8);
-  L.o_fsum = take(A.nf * Lcap * kM * 8);
-  L.o_min = take(A.has_min ? Lcap * kM * 8 : 0);
-  L.o_max = take(A.has_max ? Lcap * kM * 8 : 0);
+  L.o_isum = take(A.ni * tl * kM * 8);
+  L.o_fsum = take(A.nf * tl * kM * 8);
+  L.o_min = take(A.has_min ? tl * kM * 8 : 0);
+  L.o_max = take(A.has_max ? tl * kM * 8 : 0);
   L.o_lrows = take(Lcap * 8);
   L.o_lkey = take(L.LH * 8);
   L.o_mask = take(TS * 8);
@@ -485,7 +488,7 @@ static SmemLayout make_layout(const AccSet& A, int T, int Lcap, int key_bytes = 
   L.o_fval = take(A.nf * TS * 8);
   L.o_mval = take(mm ? TS * 8 : 0);
   L.o_rdesc = take((T / 32 + Lcap + 1) * 4);
-  L.o_cnt = take(Lcap * kM * 4);
+  L.o_cnt = take(tl * kM * 4);
   L.o_lstate = take(L.LH * 4);
   L.o_lprov = take(Lcap * 4);
   L.o_hist = take(Lcap * 4);
@@ -530,6 +533,18 @@ static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, int key_
     if (lo > best) {
       best = lo;
       bestT = T;
+    }
+  }
+  // one CTA per SM: for 33..256 slots whose accumulators fit the 512 TMEM columns, move the CTA
+  // table to TMEM (k_agg_tiles_tm) and spend the freed shared memory on 2048-row tiles
+  const int wps = 2 + 4 * A.ni + 4 * A.nf + (A.has_min ? 4 : 0) + (A.has_max ? 4 : 0);
+  if (want > 32 && 4 * ((want + 15) / 16) * wps <= kTmCols && !getenv("PAC_NO_TM")) {
+    for (int T : {2048, 1024}) {
+      SmemLayout L = make_layout(A, T, want, key_bytes, true);
+      if (L.bytes <= smem_max) {
+        *out = L;
+        return true;
+      }
     }
   }
   if (best < 1) return false;
@@ -687,6 +702,43 @@ extern template cudaError_t launch_warp<2, 2, 3>(const AggPlan&, const WarpLayou
 
 typedef cudaError_t (*LaunchFn)(const AggPlan&, const SmemLayout&, int, cudaStream_t);
 typedef cudaError_t (*LaunchWarpFn)(const AggPlan&, const WarpLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 0, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 0, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 0, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 0, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 1, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 1, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 1, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 1, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 2, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 2, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 2, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<0, 2, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 0, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 0, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 0, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 0, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 1, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 1, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 1, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 1, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 2, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 2, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 2, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<1, 2, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 0, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 0, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 0, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 0, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 1, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 1, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 1, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 1, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 2, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 2, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 2, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+extern template cudaError_t launch_tm<2, 2, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
+
 
 #define PAC_MM_ROW(NI, NF) {launch_smem<NI, NF, 0>, launch_smem<NI, NF, 1>, launch_smem<NI, NF, 2>, launch_smem<NI, NF, 3>}
 static const LaunchFn kLaunch[3][3][4] = {
@@ -700,6 +752,13 @@ static const LaunchWarpFn kLaunchWarp[3][3][4] = {
     {PAC_WMM_ROW(0, 0), PAC_WMM_ROW(0, 1), PAC_WMM_ROW(0, 2)},
     {PAC_WMM_ROW(1, 0), PAC_WMM_ROW(1, 1), PAC_WMM_ROW(1, 2)},
     {PAC_WMM_ROW(2, 0), PAC_WMM_ROW(2, 1), PAC_WMM_ROW(2, 2)},
+};
+
+#define PAC_TMM_ROW(NI, NF) {launch_tm<NI, NF, 0>, launch_tm<NI, NF, 1>, launch_tm<NI, NF, 2>, launch_tm<NI, NF, 3>}
+static const LaunchFn kLaunchTm[3][3][4] = {
+    {PAC_TMM_ROW(0, 0), PAC_TMM_ROW(0, 1), PAC_TMM_ROW(0, 2)},
+    {PAC_TMM_ROW(1, 0), PAC_TMM_ROW(1, 1), PAC_TMM_ROW(1, 2)},
+    {PAC_TMM_ROW(2, 0), PAC_TMM_ROW(2, 1), PAC_TMM_ROW(2, 2)},
 };
 
 static int device_info(int* sms, int* smem_optin) {
@@ -877,11 +936,12 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
         p.ablate = getenv("PAC_ABLATE") ? atoi(getenv("PAC_ABLATE")) : 0;
       }
       if (getenv("PAC_DEBUG"))
-        fprintf(stderr, "[libpac] k_agg_tiles<%d,%d,%d> T=%d Lcap=%d LH=%d smem=%d B (G_cap=%lld)\n", A.ni,
-                A.nf, (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0), L.T, L.Lcap, L.LH, L.bytes, (long long)G_cap);
+        fprintf(stderr, "[libpac] k_agg_tiles%s<%d,%d,%d> T=%d Lcap=%d LH=%d smem=%d B (G_cap=%lld)\n",
+                L.tm ? "_tm" : "", A.ni, A.nf, (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0), L.T, L.Lcap, L.LH, L.bytes,
+                (long long)G_cap);
       const int mm = (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0);
       profile_begin(st);
-      e = kLaunch[A.ni][A.nf][mm](p, L, sms, st);
+      e = L.tm ? kLaunchTm[A.ni][A.nf][mm](p, L, sms, st) : kLaunch[A.ni][A.nf][mm](p, L, sms, st);
       profile_end(st);
     }
     if (e != cudaSuccess) return PAC_E_CUDA;

@@ -63,6 +63,7 @@ struct SmemLayout {
   int o_mask, o_slot, o_rank, o_ucnt, o_queue, o_ival, o_rdesc, o_fval, o_mval, o_hist, o_offs,
       o_runoffs, o_xcs, o_raw, o_mbar, o_misc;
   int bytes;
+  int tm;  // 1: the CTA table lives in TMEM (k_agg_tiles_tm), no smem table
 };
 
 struct Misc {
