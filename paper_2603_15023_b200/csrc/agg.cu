@@ -511,6 +511,14 @@ static SmemLayout make_layout(const AccSet& A, int T, int Lcap, int key_bytes = 
 // fit.  PAC_TILE=512|1024 forces the tile size (experiments).
 static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, int key_bytes, SmemLayout* out) {
   const int want = (int)std::min<int64_t>(std::max<int64_t>(G_cap, 1), 256);
+  if (getenv("PAC_FORCE_TM")) {  // experiments: the TMEM-table kernel at any slot count
+    const int T = atoi(getenv("PAC_FORCE_TM")) >= 1024 ? atoi(getenv("PAC_FORCE_TM")) : 2048;
+    SmemLayout L = make_layout(A, T, want, key_bytes, true);
+    if (L.bytes <= smem_max) {
+      *out = L;
+      return true;
+    }
+  }
   const char* force = getenv("PAC_TILE");
   const int tiles_fixed[2] = {force ? atoi(force) : 1024, force ? atoi(force) : 512};  // multiples of 512
   for (int per_sm : {PAC_TILE_MINB, 3, 2}) {
