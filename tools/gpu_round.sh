@@ -1,6 +1,5 @@
 #!/bin/bash
 # one GPU session: parity suite, smoke, bench lines for every config, ncu launch list of the
-# bench command + one ncu --set full capture of k_agg_tiles (C2)
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -q --tb=short > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
@@ -8,6 +7,6 @@ tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err; tail -c 300 gpurun_out/bench_C2.json
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -c 200 gpurun_out/bench_ref.json
-for c in C1 C4 C5 C3; do timeout 900 python bench.py --config $c --steps 10 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "$c rc=$?"; done
+for c in C1 C4 C5 C3; do timeout 900 python bench.py --config $c --steps 5 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "$c rc=$?"; done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_C2.csv python bench.py --steps 20 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_agg_tiles" -s 1 -c 1 -o gpurun_out/agg_C2 -f python tools/prof_agg.py --config C2 --iters 2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+python tools/bench_m128.py > gpurun_out/bench_m128.json 2>&1; tail -1 gpurun_out/bench_m128.json
