@@ -462,55 +462,17 @@ static int raw_tile_bytes(const AccSet& A, int T, int key_bytes) {
 }
 
 static SmemLayout make_layout(const AccSet& A, int T, int Lcap, int key_bytes = 8, bool tm = false) {
-  SmemLayout L{};
-  L.tm = tm ? 1 : 0;
-  const int tl = tm ? 0 : Lcap;  // slots of the smem CTA table (none in TMEM mode)
-  L.T = T;
-  L.TS = T + 8 * Lcap;  // slot-sorted staging, each slot padded to a multiple of 8 rows
-  L.Lcap = Lcap;
-  L.LH = (int)next_pow2(std::max(4 * Lcap, 256));
-  int off = 0;
-  auto take = [&](int bytes) {
-    int o = off;
-    off += (std::max(bytes, 16) + 15) & ~15;
-    return o;
-  };
-  const bool mm = A.has_min || A.has_max;
-  const int TS = L.TS;
-  L.o_isum = take(A.ni * tl * kM * 8);
-  L.o_fsum = take(A.nf * tl * kM * 8);
-  L.o_min = take(A.has_min ? tl * kM * 8 : 0);
-  L.o_max = take(A.has_max ? tl * kM * 8 : 0);
-  L.o_lrows = take(Lcap * 8);
-  L.o_lkey = take(L.LH * 8);
-  L.o_mask = take(TS * 8);
-  L.o_ival = take(A.ni * TS * 8);
-  L.o_fval = take(A.nf * TS * 8);
-  L.o_mval = take(mm ? TS * 8 : 0);
-  L.o_rdesc = take((T / 32 + Lcap + 1) * 4);
-  L.o_cnt = take(tl * kM * 4);
-  L.o_lstate = take(L.LH * 4);
-  L.o_lprov = take(Lcap * 4);
-  L.o_hist = take(Lcap * 4);
-  L.o_offs = take(Lcap * 4);
-  L.o_runoffs = take((Lcap + 1) * 4);
-  L.o_ucnt = take((T / 32) * Lcap * 2);
-  L.o_xcs = take(32 * 16 + 32 * 8);
-  L.o_queue = take(T * 4);
-  L.o_slot = take(T * 2);
-  L.o_rank = take(T);
-  L.o_raw = take(getenv("PAC_NO_TMA") ? 0 : raw_tile_bytes(A, T, key_bytes));  // PAC_NO_TMA: rows read from HBM in A1/A2
-  L.o_mbar = take(16);
-  L.o_misc = take(sizeof(Misc));
-  L.bytes = off;
-  return L;
+  // PAC_NO_TMA: rows read from HBM in A1/A2, no staged raw tile
+  const int raw = getenv("PAC_NO_TMA") ? 0 : raw_tile_bytes(A, T, key_bytes);
+  return tile_layout(A.ni, A.nf, A.has_min, A.has_max, T, Lcap, raw, tm ? 1 : 0);
 }
 
 // Local slot capacity: min(G_cap, 256).  Preference: all wanted slots with three CTAs per SM
 // (tile 1024, then 512), then two CTAs per SM, then one CTA per SM with as many slots as
 // fit.  PAC_TILE=512|1024 forces the tile size (experiments).
 static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, int key_bytes, SmemLayout* out) {
-  const int want = (int)std::min<int64_t>(std::max<int64_t>(G_cap, 1), 256);
+  // small tables get kFixedSlots local slots: the compile-time-layout kernel instance
+  const int want = (int)std::min<int64_t>(std::max<int64_t>(G_cap, (int64_t)kFixedSlots), 256);
   if (getenv("PAC_FORCE_TM")) {  // experiments: the TMEM-table kernel at any slot count
     const int T = atoi(getenv("PAC_FORCE_TM")) >= 1024 ? atoi(getenv("PAC_FORCE_TM")) : 2048;
     SmemLayout L = make_layout(A, T, want, key_bytes, true);

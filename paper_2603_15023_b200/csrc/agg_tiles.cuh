@@ -76,6 +76,58 @@ struct Misc {
   int pad[2];
 };
 
+// Shared-memory layout of k_agg_tiles (host: agg.cu make_layout; also usable at compile time).
+__host__ __device__ constexpr int lay_take(int& off, int bytes) {
+  const int o = off;
+  off += ((bytes > 16 ? bytes : 16) + 15) & ~15;
+  return o;
+}
+__host__ __device__ constexpr int lay_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+__host__ __device__ constexpr SmemLayout tile_layout(int ni, int nf, int has_min, int has_max, int T, int Lcap,
+                                                     int raw_bytes, int tm) {
+  SmemLayout L{};
+  L.tm = tm;
+  const int tl = tm ? 0 : Lcap;  // slots of the smem CTA table (none in TMEM mode)
+  L.T = T;
+  L.TS = T + 8 * Lcap;  // slot-sorted staging, each slot padded to a multiple of 8 rows
+  L.Lcap = Lcap;
+  L.LH = lay_pow2(4 * Lcap > 256 ? 4 * Lcap : 256);
+  int off = 0;
+  const int TS = L.TS;
+  const bool mm = has_min || has_max;
+  L.o_isum = lay_take(off, ni * tl * kM * 8);
+  L.o_fsum = lay_take(off, nf * tl * kM * 8);
+  L.o_min = lay_take(off, has_min ? tl * kM * 8 : 0);
+  L.o_max = lay_take(off, has_max ? tl * kM * 8 : 0);
+  L.o_lrows = lay_take(off, Lcap * 8);
+  L.o_lkey = lay_take(off, L.LH * 8);
+  L.o_mask = lay_take(off, TS * 8);
+  L.o_ival = lay_take(off, ni * TS * 8);
+  L.o_fval = lay_take(off, nf * TS * 8);
+  L.o_mval = lay_take(off, mm ? TS * 8 : 0);
+  L.o_rdesc = lay_take(off, (T / 32 + Lcap + 1) * 4);
+  L.o_cnt = lay_take(off, tl * kM * 4);
+  L.o_lstate = lay_take(off, L.LH * 4);
+  L.o_lprov = lay_take(off, Lcap * 4);
+  L.o_hist = lay_take(off, Lcap * 4);
+  L.o_offs = lay_take(off, Lcap * 4);
+  L.o_runoffs = lay_take(off, (Lcap + 1) * 4);
+  L.o_ucnt = lay_take(off, (T / 32) * Lcap * 2);
+  L.o_xcs = lay_take(off, 32 * 16 + 32 * 8);
+  L.o_queue = lay_take(off, T * 4);
+  L.o_slot = lay_take(off, T * 2);
+  L.o_rank = lay_take(off, T);
+  L.o_mbar = lay_take(off, 16);
+  L.o_misc = lay_take(off, (int)sizeof(Misc));
+  L.o_raw = lay_take(off, raw_bytes);  // last: every other offset is independent of the columns staged
+  L.bytes = off;
+  return L;
+}
+
 // ------------------------------------------------------------------ dictionaries
 __device__ __forceinline__ void init_prov_slot(const AggPlan& p, int prov, uint64_t key) {
   p.prov_key[prov] = key;
@@ -784,8 +836,13 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
 
 // THREADS = 256: three CTAs per SM (small tables); 512: one CTA per SM with 16 warps and a
 // 128-register budget (large CTA tables, e.g. 100 groups x 3 aggregates).
-template <int NI, int NF, int MM, int THREADS>
-__global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k_agg_tiles(AggPlan p, SmemLayout L) {
+// LC = 0: the layout is the runtime parameter.  LC > 0: T = 1024 and LC local slots, the layout is
+// a compile-time constant (every smem address an immediate offset, tile/unit/slot index math
+// folded) -- the instance for small group counts (<= 8 groups, e.g. the paper's Q01 shapes).
+template <int NI, int NF, int MM, int THREADS, int LC>
+__global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k_agg_tiles(AggPlan p, SmemLayout Lp) {
+  constexpr SmemLayout Lc = tile_layout(NI, NF, MM & 1, (MM >> 1) & 1, 1024, LC > 0 ? LC : 1, 0, 0);
+  const SmemLayout& L = LC > 0 ? Lc : Lp;
   extern __shared__ __align__(16) unsigned char smem[];
   TileSmem sm;
   sm.lkey = (unsigned long long*)(smem + L.o_lkey);
@@ -967,11 +1024,15 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
 
 void note_launch();
 
+constexpr int kFixedSlots = 8;  // LC of the compile-time-layout instance
+
 template <int NI, int NF, int MM>
 cudaError_t launch_smem(const AggPlan& p, const SmemLayout& L, int sms, cudaStream_t st) {
-  // one CTA per SM -> the 16-warp variant
+  // one CTA per SM -> the 16-warp variant; T = 1024 with 8 slots -> the compile-time layout
   const bool wide = L.bytes > 232448 / 2 - 2048;
-  auto k = wide ? k_agg_tiles<NI, NF, MM, 512> : k_agg_tiles<NI, NF, MM, 256>;
+  const bool fixed = !wide && L.T == 1024 && L.Lcap == kFixedSlots && !L.tm && !getenv("PAC_NO_FIXED");
+  auto k = wide ? k_agg_tiles<NI, NF, MM, 512, 0>
+                : (fixed ? k_agg_tiles<NI, NF, MM, 256, kFixedSlots> : k_agg_tiles<NI, NF, MM, 256, 0>);
   const int threads = wide ? 512 : 256;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
   if (e != cudaSuccess) return e;

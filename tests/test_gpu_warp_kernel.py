@@ -1,4 +1,5 @@
-"""-m gpu parity of the low-cardinality path (k_agg_warp, PAC_WARP=1 and G_cap <= 8) against the
+"""-m gpu parity of the low-cardinality paths (G_cap <= 8: k_agg_warp with PAC_WARP=1, and the
+compile-time-layout instance of k_agg_tiles) against the
 CPU oracle, element by element on the same seeded inputs: BASELINE configs C1/C2 at sizes
 that span many warps and a ragged tail, plus the edge cases of that kernel -- straggler
 queue drains, partial runs, int64 values beyond the int32 tables, non-finite f64 values,
@@ -13,9 +14,15 @@ from gpu_helpers import assert_tables_equal, run_gpu, workload_aggs
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def _warp_kernel(monkeypatch):
-    monkeypatch.setenv("PAC_WARP", "1")  # k_agg_warp is opt-in
+@pytest.fixture(autouse=True, params=["warp", "tile_fixed"])
+def _kernel(request, monkeypatch):
+    """Every case runs on both low-cardinality kernels: k_agg_warp (opt-in, PAC_WARP=1) and the
+    compile-time-layout instance of k_agg_tiles (8 local slots, the default for G_cap <= 8)."""
+    if request.param == "warp":
+        monkeypatch.setenv("PAC_WARP", "1")
+    else:
+        monkeypatch.delenv("PAC_WARP", raising=False)
+    return request.param
 
 torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():  # pragma: no cover - CPU container
