@@ -2,6 +2,7 @@
 // instantiation units agg_inst_ni{0,1,2}.cu (split so the 72 kernels compile in parallel).
 #pragma once
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -632,8 +633,10 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
   constexpr int KM = 1 + NI + NF;
   constexpr int KK = 1 + NI + NF + (MM ? 1 : 0);
   TileCols<STAGED> tc{&p, sm.raw, base, T};
+  constexpr int kNoProv = INT_MIN;
   for (int li = tid; li < T; li += nth) {
     int s = -1;
+    int gprov = kNoProv;  // provisional HBM slot of a row without a local slot (-1: no capacity)
     if (li < tn) {
       bool keep = true;
       if (p.mask_in) keep = tc.w8(0, li) != 0ull;  // R21: a row in no world is dropped
@@ -642,16 +645,39 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
         const int code = local_code(p, key, sm.lkey, sm.lstate, LH, sm.lprov, Lcap, sm.misc);
         if (code < kOvfBase) {
           s = code - 1;
-        } else {  // no local slot: straight to the HBM table (rare)
-          long long iv[NI > 0 ? NI : 1];
-          double fv[NF > 0 ? NF : 1];
+        } else {  // no local slot: the HBM tier, below
+          gprov = code - kOvfBase - 1;
+        }
+      }
+    }
+    // HBM tier (groups without a CTA-local slot, e.g. the long tail of C3): the warp applies
+    // each such row cooperatively -- lane j updates worlds j and j+32, so the 64 world
+    // updates of a row are coalesced device atomics on consecutive addresses
+    unsigned gp = __ballot_sync(0xffffffffu, gprov != kNoProv);
+    if (gp) {
+      uint64_t gm = 0;
+      if (gprov != kNoProv) gm = p.mask_in ? tc.w8(0, li) : pac_hash_dev(tc.w8(0, li), p.salt);
+      while (gp) {
+        const int src = __ffs(gp) - 1;
+        gp &= gp - 1;
+        const int prov = __shfl_sync(0xffffffffu, gprov, src);
+        const uint64_t m = __shfl_sync(0xffffffffu, gm, src);
+        const int lsrc = (li & ~31) + src;
+        if (lane == 0) atomicAdd(&p.dbg[0], 1ull);
+        if (prov < 0) continue;  // capacity exhausted: reported by the finish kernel
+        if (lane == 0) atomicAdd(&p.prov_rows[prov], 1ull);
+        const size_t b = (size_t)prov * kM;
 #pragma unroll
-          for (int c = 0; c < NI; ++c) iv[c] = (long long)tc.w8(1 + c, li);
+        for (int h = 0; h < 2; ++h) {
+          const int j = lane + 32 * h;
+          if (!((m >> j) & 1ull)) continue;
+          if (p.has_count) atomicAdd(&p.prov_count[b + j], 1ull);
 #pragma unroll
-          for (int c = 0; c < NF; ++c) fv[c] = __longlong_as_double((long long)tc.w8(KF + c, li));
-          const double mv = MM ? __longlong_as_double((long long)tc.w8(KM, li)) : 0.0;
-          const uint64_t m = p.mask_in ? tc.w8(0, li) : pac_hash_dev(tc.w8(0, li), p.salt);
-          global_row_update<NI, NF, MM>(p, code - kOvfBase - 1, m, iv, fv, mv);
+          for (int c = 0; c < NI; ++c) atomicAdd(&p.prov_isum[c][b + j], (unsigned long long)tc.w8(1 + c, lsrc));
+#pragma unroll
+          for (int c = 0; c < NF; ++c) atomicAdd(&p.prov_fsum[c][b + j], __longlong_as_double((long long)tc.w8(KF + c, lsrc)));
+          if (MM & 1) atomicMin(&p.prov_min[b + j], enc_f64(__longlong_as_double((long long)tc.w8(KM, lsrc))));
+          if (MM & 2) atomicMax(&p.prov_max[b + j], enc_f64(__longlong_as_double((long long)tc.w8(KM, lsrc))));
         }
       }
     }
@@ -878,7 +904,6 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
   const int tid = threadIdx.x, nth = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
   const int T = L.T, Lcap = L.Lcap, LH = L.LH;
-  const int units = T >> 5;
 
   for (int i = tid; i < LH; i += nth) sm.lstate[i] = 0;
   for (int i = tid; i < Lcap; i += nth) {
