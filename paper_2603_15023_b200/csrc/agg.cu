@@ -19,7 +19,6 @@
 #include <vector>
 
 #include "agg_tiles.cuh"
-#include "agg_warp.cuh"
 #include "agg_tm.cuh"
 
 namespace pac {
@@ -549,50 +548,6 @@ static MMLayout mm_layout(int64_t G_cap, int smem_max) {
   return L;
 }
 
-static WarpLayout warp_layout(const AccSet& A, int Lw, int nw) {
-  WarpLayout L{};
-  L.Lw = Lw;
-  L.nw = nw;
-  L.LH = (int)next_pow2(std::max(4 * Lw, 256));
-  const bool mm = A.has_min || A.has_max;
-  int off = 0;
-  auto take = [&](int bytes) {
-    int o = off;
-    off += (std::max(bytes, 16) + 15) & ~15;
-    return o;
-  };
-  L.o_lkey = take(L.LH * 8);
-  L.o_isum = take(A.ni * Lw * kM * 8);
-  L.o_fsum = take(A.nf * Lw * kM * 8);
-  L.o_min = take(A.has_min ? Lw * kM * 8 : 0);
-  L.o_max = take(A.has_max ? Lw * kM * 8 : 0);
-  L.o_cnt = take(Lw * kM * 4);
-  L.o_lstate = take(L.LH * 4);
-  L.o_lprov = take(Lw * 4);
-  L.o_lrows = take(Lw * 4);
-  L.o_misc = take(sizeof(Misc));
-  L.o_warp = off;
-  int w = 0;
-  auto wtake = [&](int bytes) {
-    int o = w;
-    w += (std::max(bytes, 16) + 15) & ~15;
-    return o;
-  };
-  L.w_mask = wtake(Lw * kWarpCap * 8);
-  L.w_ival = wtake(A.ni * Lw * kWarpCap * 8);
-  L.w_fval = wtake(A.nf * Lw * kWarpCap * 8);
-  L.w_mval = wtake(mm ? Lw * kWarpCap * 8 : 0);
-  L.w_qw0 = wtake(kWarpQueue * 8);
-  L.w_qm = wtake(kWarpQueue * 8);
-  L.w_qival = wtake(A.ni * kWarpQueue * 8);
-  L.w_qfval = wtake(A.nf * kWarpQueue * 8);
-  L.w_qmval = wtake(mm ? kWarpQueue * 8 : 0);
-  L.w_qslot = wtake(kWarpQueue * 4);
-  L.w_cnt = wtake(Lw * 4);
-  L.warp_bytes = w;
-  L.bytes = off + nw * w;
-  return L;
-}
 
 // instantiated in agg_inst_ni{0,1,2}.cu
 
@@ -633,45 +588,8 @@ extern template cudaError_t launch_smem<2, 2, 1>(const AggPlan&, const SmemLayou
 extern template cudaError_t launch_smem<2, 2, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
 extern template cudaError_t launch_smem<2, 2, 3>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
 
-extern template cudaError_t launch_warp<0, 0, 0>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 0, 1>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 0, 2>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 0, 3>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 1, 0>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 1, 1>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 1, 2>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 1, 3>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 2, 0>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 2, 1>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 2, 2>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<0, 2, 3>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 0, 0>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 0, 1>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 0, 2>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 0, 3>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 1, 0>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 1, 1>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 1, 2>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 1, 3>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 2, 0>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 2, 1>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 2, 2>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<1, 2, 3>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 0, 0>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 0, 1>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 0, 2>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 0, 3>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 1, 0>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 1, 1>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 1, 2>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 1, 3>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 2, 0>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 2, 1>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 2, 2>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
-extern template cudaError_t launch_warp<2, 2, 3>(const AggPlan&, const WarpLayout&, int, cudaStream_t);
 
 typedef cudaError_t (*LaunchFn)(const AggPlan&, const SmemLayout&, int, cudaStream_t);
-typedef cudaError_t (*LaunchWarpFn)(const AggPlan&, const WarpLayout&, int, cudaStream_t);
 extern template cudaError_t launch_tm<0, 0, 0>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
 extern template cudaError_t launch_tm<0, 0, 1>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
 extern template cudaError_t launch_tm<0, 0, 2>(const AggPlan&, const SmemLayout&, int, cudaStream_t);
@@ -717,12 +635,6 @@ static const LaunchFn kLaunch[3][3][4] = {
     {PAC_MM_ROW(2, 0), PAC_MM_ROW(2, 1), PAC_MM_ROW(2, 2)},
 };
 
-#define PAC_WMM_ROW(NI, NF) {launch_warp<NI, NF, 0>, launch_warp<NI, NF, 1>, launch_warp<NI, NF, 2>, launch_warp<NI, NF, 3>}
-static const LaunchWarpFn kLaunchWarp[3][3][4] = {
-    {PAC_WMM_ROW(0, 0), PAC_WMM_ROW(0, 1), PAC_WMM_ROW(0, 2)},
-    {PAC_WMM_ROW(1, 0), PAC_WMM_ROW(1, 1), PAC_WMM_ROW(1, 2)},
-    {PAC_WMM_ROW(2, 0), PAC_WMM_ROW(2, 1), PAC_WMM_ROW(2, 2)},
-};
 
 #define PAC_TMM_ROW(NI, NF) {launch_tm<NI, NF, 0>, launch_tm<NI, NF, 1>, launch_tm<NI, NF, 2>, launch_tm<NI, NF, 3>}
 static const LaunchFn kLaunchTm[3][3][4] = {
@@ -868,15 +780,6 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
       k_agg_minmax<<<grid, kThreads, L.bytes, st>>>(p, L);
       note_launch();
       e = cudaGetLastError();
-      profile_end(st);
-    } else if (G_cap <= kWarpSlots && getenv("PAC_WARP")) {
-      // low cardinality, opt-in (PAC_WARP=1): warp-independent kernel (agg_warp.cuh)
-      const WarpLayout L = warp_layout(A, (int)G_cap, kWarpThreads / 32);
-      if (L.bytes > smem_max) return PAC_E_INVAL;
-      p.raw_src[0] = d_mask ? (const void*)d_mask : (const void*)d_pu_key;
-      const int mm = (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0);
-      profile_begin(st);
-      e = kLaunchWarp[A.ni][A.nf][mm](p, L, sms, st);
       profile_end(st);
     } else {
       SmemLayout L{};

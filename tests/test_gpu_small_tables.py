@@ -1,10 +1,9 @@
-"""-m gpu parity of the low-cardinality paths (G_cap <= 8: k_agg_warp with PAC_WARP=1, and the
-compile-time-layout instance of k_agg_tiles) against the
-CPU oracle, element by element on the same seeded inputs: BASELINE configs C1/C2 at sizes
-that span many warps and a ragged tail, plus the edge cases of that kernel -- straggler
-queue drains, partial runs, int64 values beyond the int32 tables, non-finite f64 values,
-MIN/MAX next to COUNT, explicit (reduced / zero) masks, the HBM-tier fallback when more keys
-than local slots appear, and the A/B switch to the tile kernel (PAC_WARP unset)."""
+"""-m gpu parity of the small-table path (G_cap <= 8: the compile-time-layout instance of
+k_agg_tiles, 8 local slots) against the CPU oracle, element by element on the same seeded
+inputs: BASELINE configs C1/C2 at sizes that span many CTAs and a ragged tail, plus the edge
+cases -- straggler queues, partial runs, int64 values beyond the int32 tables, non-finite f64
+values, MIN/MAX next to COUNT, explicit (reduced / zero) masks, capacity overflow, and the A/B
+switch to the runtime-layout instance (PAC_NO_FIXED)."""
 import numpy as np
 import pytest
 
@@ -13,16 +12,6 @@ from gpu_helpers import assert_tables_equal, run_gpu, workload_aggs
 
 pytestmark = pytest.mark.gpu
 
-
-@pytest.fixture(autouse=True, params=["warp", "tile_fixed"])
-def _kernel(request, monkeypatch):
-    """Every case runs on both low-cardinality kernels: k_agg_warp (opt-in, PAC_WARP=1) and the
-    compile-time-layout instance of k_agg_tiles (8 local slots, the default for G_cap <= 8)."""
-    if request.param == "warp":
-        monkeypatch.setenv("PAC_WARP", "1")
-    else:
-        monkeypatch.delenv("PAC_WARP", raising=False)
-    return request.param
 
 torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():  # pragma: no cover - CPU container
@@ -94,7 +83,7 @@ def test_explicit_masks_with_zeros(orc):
     assert_tables_equal(t.to_host(), orc.agg(masks, keys, aggs))
 
 
-def test_capacity_exceeded_reported_by_warp_kernel():
+def test_capacity_exceeded_reported():
     import paper_2603_15023_b200 as pac
     from gpu_helpers import to_dev
     n = 20_000
@@ -107,13 +96,12 @@ def test_capacity_exceeded_reported_by_warp_kernel():
     assert e.value.rc == 2
 
 
-def test_warp_and_tile_kernels_agree(orc, monkeypatch):
+def test_fixed_and_runtime_layouts_agree(orc, monkeypatch):
     w = dg.WORKLOADS["C2"]
     cols = w.host_columns(0, 400_000)
     aggs = workload_aggs(w, cols)
     t1, _ = run_gpu(aggs, cols["keys"], pu=cols["pu"], salt=SALT, G_cap=8)
     a = t1.to_host()
-    monkeypatch.delenv("PAC_WARP", raising=False)
+    monkeypatch.setenv("PAC_NO_FIXED", "1")
     t2, _ = run_gpu(aggs, cols["keys"], pu=cols["pu"], salt=SALT, G_cap=8)
-    b = t2.to_host()
-    assert_tables_equal(a, b)
+    assert_tables_equal(a, t2.to_host())
