@@ -50,7 +50,7 @@ def build_cuda(name: str, force: bool = False, verbose: bool = False) -> str:
         return src, obj, r
 
     from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+    with ThreadPoolExecutor(max_workers=min(os.cpu_count() or 8, len(srcs))) as ex:
         results = list(ex.map(compile_one, srcs))
     for src, obj, r in results:
         if r.returncode != 0:

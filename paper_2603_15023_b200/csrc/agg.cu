@@ -507,9 +507,12 @@ static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, int key_
   // one CTA per SM: for 33..256 slots whose accumulators fit the 512 TMEM columns, move the CTA
   // table to TMEM (k_agg_tiles_tm) and spend the freed shared memory on 2048-row tiles
   const int wps = 2 + 4 * A.ni + 4 * A.nf + (A.has_min ? 4 : 0) + (A.has_max ? 4 : 0);
-  if (want > 32 && 4 * ((want + 15) / 16) * wps <= kTmCols && !getenv("PAC_NO_TM")) {
+  // 65..128 slots are rounded up to the compile-time TMEM instance (kTmFixedSlots, T = 2048)
+  const int want_tm = (want > 64 && want <= kTmFixedSlots && 4 * (kTmFixedSlots / 16) * wps <= kTmCols)
+                          ? kTmFixedSlots : want;
+  if (want > 32 && 4 * ((want_tm + 15) / 16) * wps <= kTmCols && !getenv("PAC_NO_TM")) {
     for (int T : {2048, 1024}) {
-      SmemLayout L = make_layout(A, T, want, key_bytes, true);
+      SmemLayout L = make_layout(A, T, want_tm, key_bytes, true);
       if (L.bytes <= smem_max) {
         *out = L;
         return true;

@@ -153,8 +153,14 @@ __device__ __forceinline__ void tm_to_hbm(const AggPlan& p, uint32_t a, int prov
   }
 }
 
-template <int NI, int NF, int MM>
-__global__ void __launch_bounds__(kTmThreads, 1) k_agg_tiles_tm(AggPlan p, SmemLayout L) {
+// LC = 0: runtime layout; LC > 0: T = 2048 with LC local slots as a compile-time layout (as
+// k_agg_tiles' small-table instance: immediate smem offsets, folded index arithmetic).
+constexpr int kTmFixedSlots = 128;
+
+template <int NI, int NF, int MM, int LC>
+__global__ void __launch_bounds__(kTmThreads, 1) k_agg_tiles_tm(AggPlan p, SmemLayout Lp) {
+  constexpr SmemLayout Lc = tile_layout(NI, NF, MM & 1, (MM >> 1) & 1, 2048, LC > 0 ? LC : 1, 0, 1);
+  const SmemLayout& L = LC > 0 ? Lc : Lp;
   using S = TmSlot<NI, NF, MM>;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t s_tbase;
@@ -323,7 +329,8 @@ constexpr int tm_cols_needed(int Lcap) {
 
 template <int NI, int NF, int MM>
 cudaError_t launch_tm(const AggPlan& p, const SmemLayout& L, int sms, cudaStream_t st) {
-  auto k = k_agg_tiles_tm<NI, NF, MM>;
+  const bool fixed = L.T == 2048 && L.Lcap == kTmFixedSlots && !getenv("PAC_NO_FIXED");
+  auto k = fixed ? k_agg_tiles_tm<NI, NF, MM, kTmFixedSlots> : k_agg_tiles_tm<NI, NF, MM, 0>;
   if (tm_cols_needed<NI, NF, MM>(L.Lcap) > kTmCols) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
   if (e != cudaSuccess) return e;
