@@ -38,63 +38,121 @@ struct MMLayout {
   int bytes;
 };
 
-__global__ void __launch_bounds__(kThreads) k_agg_minmax(AggPlan p, MMLayout L) {
+// Rows per thread per tile: their loads are all issued before any is used, so a thread keeps
+// kMMRows independent row loads in flight (the pruned path is memory-latency bound otherwise).
+#ifndef PAC_MM_ROWS
+#define PAC_MM_ROWS 4
+#endif
+constexpr int kMMRows = PAC_MM_ROWS;
+
+// candidate mask (rare: rows that can still improve a bound) -- out of line, so the 8-row
+// unrolled scan stays small in the instruction cache
+__device__ __noinline__ uint64_t mm_candidate_mask(uint64_t key, uint64_t salt) { return pac_hash_dev(key, salt); }
+
+// refresh the cached bounds of slot s from the HBM table (one warp)
+__device__ __forceinline__ void mm_refresh(const AggPlan& p, int pv, int s, long long* bmin, long long* bmax,
+                                           int lane) {
+  const size_t b = (size_t)pv * kM;
+  if (p.has_max) {
+    long long a = min(*(volatile long long*)&p.prov_max[b + lane], *(volatile long long*)&p.prov_max[b + lane + 32]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, d));
+    if (lane == 0) bmax[s] = a;
+  }
+  if (p.has_min) {
+    long long a = max(*(volatile long long*)&p.prov_min[b + lane], *(volatile long long*)&p.prov_min[b + lane + 32]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) a = max(a, __shfl_xor_sync(0xffffffffu, a, d));
+    if (lane == 0) bmin[s] = a;
+  }
+}
+
+// No CTA barrier in the row loop: the cached bounds only have to be some value the HBM table
+// held (a stale bound admits extra candidates, never a wrong result), so each warp refreshes
+// the slots it updated itself, after its tile, from a per-warp dirty bitmap.
+#ifndef PAC_MM_MINB
+#define PAC_MM_MINB 2
+#endif
+__global__ void __launch_bounds__(kThreads, PAC_MM_MINB) k_agg_minmax(AggPlan p, MMLayout L) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* lkey = (unsigned long long*)(smem + L.o_lkey);
   int* lstate = (int*)(smem + L.o_lstate);
   int* lprov = (int*)(smem + L.o_lprov);
-  unsigned long long* lrows = (unsigned long long*)(smem + L.o_lrows);
+  unsigned* lrows = (unsigned*)(smem + L.o_lrows);
   long long* bmin = (long long*)(smem + L.o_bmin);  // max_j MIN_j (enc), cached
   long long* bmax = (long long*)(smem + L.o_bmax);  // min_j MAX_j (enc), cached
-  int* dirty = (int*)(smem + L.o_dirty);
   Misc* misc = (Misc*)(smem + L.o_misc);
-  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int Lcap = L.Lcap, LH = L.LH;
+  const int nwords = (Lcap + 31) >> 5;
+  unsigned* wdirty = (unsigned*)(smem + L.o_dirty) + wid * nwords;  // this warp's dirty slots
 
   for (int i = tid; i < LH; i += nth) lstate[i] = 0;
   for (int i = tid; i < Lcap; i += nth) {
     lrows[i] = 0;
     bmin[i] = kEncPosInf;   // nothing can be pruned until every world holds a value
     bmax[i] = kEncNegInf;
-    dirty[i] = 0;
   }
+  for (int i = lane; i < nwords; i += 32) wdirty[i] = 0u;
   if (tid == 0) {
     misc->nlocal = 0;
     misc->ndict = 0;
   }
   __syncthreads();
 
-  const int T = nth * 4;
+  const int T = nth * kMMRows;
   const int64_t ntiles = (p.n_rows + T - 1) / T;
   const int64_t t_per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * t_per;
   const int64_t t1 = min(ntiles, t0 + t_per);
 
+#pragma unroll 1
   for (int64_t tile = t0; tile < t1; ++tile) {
     const int64_t base = tile * T;
-#pragma unroll 1
-    for (int k = 0; k < 4; ++k) {
+    // all loads of the tile's rows first (kMMRows per thread in flight)
+    double vv[kMMRows];
+    uint64_t kk[kMMRows], mk[kMMRows];
+#pragma unroll
+    for (int k = 0; k < kMMRows; ++k) {
       const int64_t r = base + k * nth + tid;
-      bool valid = r < p.n_rows;
+      const bool in = r < p.n_rows;
+      vv[k] = in ? __ldcs(p.mcol + r) : 0.0;
+      mk[k] = (in && p.mask_in) ? __ldcs((const unsigned long long*)p.mask_in + r) : (in ? ~0ull : 0ull);
+      kk[k] = 0ull;
+    }
+    // group keys column by column (R20), the kMMRows loads of a column issued back to back
+    for (int c = 0; c < p.n_keys; ++c) {
+      const int w = p.key_bytes[c];
+      const void* col = p.key_col[c];
+      uint64_t kv[kMMRows];
+#pragma unroll
+      for (int k = 0; k < kMMRows; ++k) {
+        const int64_t r = min(base + k * nth + tid, p.n_rows - 1);
+        kv[k] = w == 1 ? (uint64_t)(uint8_t)__ldcs((const signed char*)col + r)
+              : w == 2 ? (uint64_t)(uint16_t)__ldcs((const short*)col + r)
+              : w == 4 ? (uint64_t)(uint32_t)__ldcs((const int*)col + r)
+                       : (uint64_t)__ldcs((const long long*)col + r);
+      }
+#pragma unroll
+      for (int k = 0; k < kMMRows; ++k) {
+        const uint64_t v = kv[k] ^ (1ull << (8 * w - 1));
+        kk[k] = (w == 8) ? v : ((kk[k] << (8 * w)) | v);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kMMRows; ++k) {
+      const int64_t r = base + k * nth + tid;
+      const bool valid = r < p.n_rows && mk[k] != 0;  // R21: a row in no world creates no group
       bool cand = false;
-      uint64_t m = 0;
-      double v = 0.0;
+      const double v = vv[k];
       int prov = -1, s = -1;
       if (valid) {
-        if (p.mask_in) {
-          m = __ldg(p.mask_in + r);
-          valid = m != 0;  // R21: a row in no world creates no group
-        }
-      }
-      if (valid) {
-        v = __ldg(p.mcol + r);
         const long long e = enc_f64(v);
-        const uint64_t key = row_group_key(p, r);
-        const int code = local_code(p, key, lkey, lstate, LH, lprov, Lcap, misc);
+        const int code = local_code(p, kk[k], lkey, lstate, LH, lprov, Lcap, misc);
         if (code < kOvfBase) {
           s = code - 1;
           prov = lprov[s];
-          atomicAdd(&lrows[s], 1ull);
+          atomicAdd(&lrows[s], 1u);
           cand = (p.has_max && e > bmax[s]) || (p.has_min && e < bmin[s]);
         } else {
           prov = code - kOvfBase - 1;
@@ -102,60 +160,57 @@ __global__ void __launch_bounds__(kThreads) k_agg_minmax(AggPlan p, MMLayout L) 
           cand = true;
         }
         if (prov < 0) cand = false;
-        if (cand && !p.mask_in) m = pac_hash_dev((uint64_t)__ldg(p.pu_key + r), p.salt);
       }
       // warp-cooperative world update of the candidate rows (lane l: worlds l, l+32)
       unsigned cm = __ballot_sync(0xffffffffu, cand);
-      while (cm) {
-        const int src = __ffs(cm) - 1;
-        cm &= cm - 1;
-        const uint64_t mm = __shfl_sync(0xffffffffu, m, src);
-        const double vv = __shfl_sync(0xffffffffu, v, src);
-        const int pv = __shfl_sync(0xffffffffu, prov, src);
-        const int ss = __shfl_sync(0xffffffffu, s, src);
-        const long long e = enc_f64(vv);
-        const size_t b = (size_t)pv * kM;
-        if ((mm >> lane) & 1ull) {
-          if (p.has_max) atomicMax(&p.prov_max[b + lane], e);
-          if (p.has_min) atomicMin(&p.prov_min[b + lane], e);
-        }
-        if ((mm >> (lane + 32)) & 1ull) {
-          if (p.has_max) atomicMax(&p.prov_max[b + lane + 32], e);
-          if (p.has_min) atomicMin(&p.prov_min[b + lane + 32], e);
-        }
-        if (lane == 0 && ss >= 0) dirty[ss] = 1;
-      }
-    }
-    __syncthreads();
-    // refresh the bounds of the slots that received candidates (warp per slot)
-    const int nloc = min(misc->nlocal, Lcap);
-    for (int s = wid; s < nloc; s += nw) {
-      if (!dirty[s]) continue;
-      const int pv = lprov[s];
-      if (pv >= 0) {
-        const size_t b = (size_t)pv * kM;
-        if (p.has_max) {
-          long long a = min(*(volatile long long*)&p.prov_max[b + lane],
-                            *(volatile long long*)&p.prov_max[b + lane + 32]);
-#pragma unroll
-          for (int d = 16; d > 0; d >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, d));
-          if (lane == 0) bmax[s] = a;
-        }
-        if (p.has_min) {
-          long long a = max(*(volatile long long*)&p.prov_min[b + lane],
-                            *(volatile long long*)&p.prov_min[b + lane + 32]);
-#pragma unroll
-          for (int d = 16; d > 0; d >>= 1) a = max(a, __shfl_xor_sync(0xffffffffu, a, d));
-          if (lane == 0) bmin[s] = a;
+      if (cm) {
+        uint64_t m = mk[k];
+        if (cand && !p.mask_in) m = mm_candidate_mask((uint64_t)__ldg(p.pu_key + r), p.salt);
+        while (cm) {
+          const int src = __ffs(cm) - 1;
+          cm &= cm - 1;
+          const uint64_t mm = __shfl_sync(0xffffffffu, m, src);
+          const double vs = __shfl_sync(0xffffffffu, v, src);
+          const int pv = __shfl_sync(0xffffffffu, prov, src);
+          const int ss = __shfl_sync(0xffffffffu, s, src);
+          const long long e = enc_f64(vs);
+          const size_t b = (size_t)pv * kM;
+          if ((mm >> lane) & 1ull) {
+            if (p.has_max) atomicMax(&p.prov_max[b + lane], e);
+            if (p.has_min) atomicMin(&p.prov_min[b + lane], e);
+          }
+          if ((mm >> (lane + 32)) & 1ull) {
+            if (p.has_max) atomicMax(&p.prov_max[b + lane + 32], e);
+            if (p.has_min) atomicMin(&p.prov_min[b + lane + 32], e);
+          }
+          if (lane == 0 && ss >= 0) wdirty[ss >> 5] |= 1u << (ss & 31);
         }
       }
-      if (lane == 0) dirty[s] = 0;
     }
-    __syncthreads();
+    __syncwarp();
+    // this warp refreshes the bounds of the slots it updated (no CTA barrier)
+    for (int wb = 0; wb < nwords; wb += 32) {
+      const unsigned bits = wb + lane < nwords ? wdirty[wb + lane] : 0u;
+      unsigned have = __ballot_sync(0xffffffffu, bits != 0u);
+      while (have) {
+        const int src = __ffs(have) - 1;
+        have &= have - 1;
+        unsigned wbits = __shfl_sync(0xffffffffu, bits, src);
+        while (wbits) {
+          const int s = ((wb + src) << 5) + __ffs(wbits) - 1;
+          wbits &= wbits - 1;
+          const int pv = lprov[s];
+          if (pv >= 0) mm_refresh(p, pv, s, bmin, bmax, lane);
+        }
+      }
+      if (bits) wdirty[wb + lane] = 0u;
+    }
+    __syncwarp();
   }
+  __syncthreads();
   const int nloc = min(misc->nlocal, Lcap);
   for (int s = tid; s < nloc; s += nth)
-    if (lprov[s] >= 0 && lrows[s]) atomicAdd(&p.prov_rows[lprov[s]], lrows[s]);
+    if (lprov[s] >= 0 && lrows[s]) atomicAdd(&p.prov_rows[lprov[s]], (unsigned long long)lrows[s]);
 }
 
 // ------------------------------------------------------------------ finish: count, sort, gather
@@ -529,7 +584,10 @@ static MMLayout mm_layout(int64_t G_cap, int smem_max) {
   int Lcap = (int)std::min<int64_t>(std::max<int64_t>(G_cap, 1), 4096);
   for (;;) {
     L.Lcap = Lcap;
-    L.LH = (int)next_pow2(std::max(4 * Lcap, 256));
+#ifndef PAC_MM_LH
+#define PAC_MM_LH 4
+#endif
+    L.LH = (int)next_pow2(std::max(PAC_MM_LH * Lcap, 256));
     int off = 0;
     auto take = [&](int bytes) {
       int o = off;
@@ -537,12 +595,12 @@ static MMLayout mm_layout(int64_t G_cap, int smem_max) {
       return o;
     };
     L.o_lkey = take(L.LH * 8);
-    L.o_lrows = take(Lcap * 8);
+    L.o_lrows = take(Lcap * 4);
     L.o_bmin = take(Lcap * 8);
     L.o_bmax = take(Lcap * 8);
     L.o_lstate = take(L.LH * 4);
     L.o_lprov = take(Lcap * 4);
-    L.o_dirty = take(Lcap * 4);
+    L.o_dirty = take((kThreads / 32) * ((Lcap + 31) / 32) * 4);  // per-warp dirty bitmaps
     L.o_misc = take(sizeof(Misc));
     L.bytes = off;
     if (L.bytes <= smem_max || Lcap == 1) break;
@@ -777,7 +835,7 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_agg_minmax, kThreads, L.bytes);
       per_sm = std::max(1, per_sm);
-      int64_t tiles = (n_rows + kThreads * 4 - 1) / (kThreads * 4);
+      int64_t tiles = (n_rows + kThreads * kMMRows - 1) / (kThreads * kMMRows);
       int grid = (int)std::min<int64_t>(tiles, (int64_t)sms * per_sm);
       profile_begin(st);
       k_agg_minmax<<<grid, kThreads, L.bytes, st>>>(p, L);
