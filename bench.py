@@ -103,6 +103,7 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------------- CPU legs
 def oracle_rows_per_s(w, budget_s: float = 12.0, max_rows: int = 4_000_000):
+    max_rows = min(max_rows, w.n_rows)
     """The CPU oracle (as it stands) on a bounded sample of the workload: rows/s."""
     import numpy as np
 
@@ -111,7 +112,7 @@ def oracle_rows_per_s(w, budget_s: float = 12.0, max_rows: int = 4_000_000):
     seed = 0xC0FFEE
     jstar, salt, P = oracle.session(seed)
     # calibrate on a small prefix, then size the sample for ~budget_s of CPU work
-    n0 = 100_000
+    n0 = min(100_000, max_rows)
     cols = w.host_columns(0, n0)
     aggs = [(k, None if i < 0 else cols["values"][i]) for k, i in w.aggs]
     t = time.perf_counter()
@@ -136,7 +137,8 @@ def run_reference(args, w):
     steps_val = []
     sample = None
     for i in range(args.warmup + args.steps):
-        v, n, el = oracle_rows_per_s(w, budget_s=max(2.0, 60.0 / max(1, args.warmup + args.steps)),
+        v, n, el = oracle_rows_per_s(w, budget_s=max(min(2.0, args.ref_seconds),
+                                                     args.ref_seconds / max(1, args.warmup + args.steps)),
                                      max_rows=2_000_000)
         if i >= args.warmup:
             steps_val.append(v)
@@ -168,6 +170,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=60.0,
+                    help="--impl reference: total CPU seconds the oracle samples take")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
