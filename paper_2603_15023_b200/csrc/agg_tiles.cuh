@@ -18,7 +18,12 @@ constexpr int kTileThreads = 256;  // k_agg_tiles
 #ifndef PAC_TILE_MINB
 #define PAC_TILE_MINB 3  // min resident CTAs per SM the register allocation targets
 #endif
-constexpr int kOvfBase = 0x20000000;  // local-dict code for keys without a local slot
+constexpr int kOvfBase = 0x20000000;
+#ifdef PAC_ABLATE_BUILD
+constexpr bool kAblate = true;   // profiling build: PAC_ABLATE switches phases off
+#else
+constexpr bool kAblate = false;
+#endif  // local-dict code for keys without a local slot
 constexpr int kSmallSort = 4096;      // single-CTA bitonic sort up to this many groups
 
 struct AggPlan {
@@ -43,7 +48,7 @@ struct AggPlan {
   // raw input columns staged per tile by 1-D TMA bulk copies (k_agg_tiles):
   // 0 = pu_key or mask, 1..n_keys = key columns, then int64 sums, f64 sums, min/max column
   int nraw, tma_ok;
-  int ablate;  // profiling only (PAC_ABLATE): 1 = no draws, 2 = no A3, 4 = no phase C
+  int ablate;  // profiling builds only (-DPAC_ABLATE_BUILD, env PAC_ABLATE): 1 = no draws, 2 = no A3, 4 = no phase C
   const void* raw_src[1 + PAC_MAX_KEYS + 5];
   int raw_eb[1 + PAC_MAX_KEYS + 5];
   int raw_off[1 + PAC_MAX_KEYS + 5];  // byte offset of the column inside the raw tile buffer
@@ -780,7 +785,8 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
 
   // ---------------- A2: hash word 0 (two rows per thread, interleaved) + values, written
   // straight to the slot-sorted position; rows still needing flips go to the warp's queue.
-  bool big = false, nonfin = false;
+  unsigned long long tmax = 0;  // max |int64 value| of this thread's rows of the tile
+  uint32_t emax = 0;            // max f64 exponent field (0x7FF00000 = inf/nan) of its rows
   unsigned short* qpos = sm.qpos + wid * (T / nw);
   unsigned short* qrow = sm.qrow + wid * (T / nw);
   int qn = 0;
@@ -795,7 +801,7 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
     uint64_t ma = ka, mb = kb;
     if (!p.mask_in) {
       HashState ha, hb;
-      if (p.ablate & 1) {
+      if (kAblate && (p.ablate & 1)) {
         ha.x = ka; ha.cand = ka; ha.k = 0; hb.x = kb; hb.cand = kb; hb.k = 0;
       } else {
         pac_hash_begin2(ka, kb, p.salt, ha, hb);
@@ -818,14 +824,13 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
       for (int c = 0; c < NI; ++c) {
         const long long v = (long long)tc.w8(1 + c, li);
         const unsigned long long a = v < 0 ? 0ull - (unsigned long long)v : (unsigned long long)v;
-        maxabs = a > maxabs ? a : maxabs;
-        big |= a >= (1ull << 26);
+        tmax = a > tmax ? a : tmax;
         sm.sival[c * TS + pos] = v;
       }
 #pragma unroll
       for (int c = 0; c < NF; ++c) {
         const double v = __longlong_as_double((long long)tc.w8(KF + c, li));
-        nonfin |= !finite_bits(v);
+        emax = max(emax, (uint32_t)__double2hiint(v) & 0x7FF00000u);
         sm.sfval[c * TS + pos] = v;
       }
       if (MM) sm.smval[pos] = __longlong_as_double((long long)tc.w8(KM, li));
@@ -842,13 +847,14 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
       qn += __popc(pm);
     }
   }
-  if (NI > 0 && __any_sync(0xffffffffu, big) && lane == 0) misc->big = 1;
-  if (NF > 0 && __any_sync(0xffffffffu, nonfin) && lane == 0) misc->nonfinite = 1;
+  maxabs = tmax > maxabs ? tmax : maxabs;
+  if (NI > 0 && __any_sync(0xffffffffu, tmax >= (1ull << 26)) && lane == 0) misc->big = 1;
+  if (NF > 0 && __any_sync(0xffffffffu, emax == 0x7FF00000u) && lane == 0) misc->nonfinite = 1;
   __syncwarp();
 
   // ---------------- A3: the warp finishes its own queued masks from draw word 1 on (state
   // re-derived from the partial mask, R2; word 0 from the staged key slot, or recomputed).
-  if (!(p.ablate & 2)) {
+  if (!(kAblate && (p.ablate & 2))) {
     for (int qi = lane; qi < qn; qi += 32) {
       const int pos = qpos[qi];
       const int li = qrow[qi];
@@ -967,7 +973,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
     if (tid == 0 && next_staged) issue_tile(p, raw, mbar, (tile + 1) * T, T);
 
     // ---------------- C: world-parallel runs, transposed "Four Russians" tables
-    if (!(p.ablate & 4)) {
+    if (!(kAblate && (p.ablate & 4))) {
       RunCtx x;
       x.smask = sm.smask;
       x.sival = sm.sival;
