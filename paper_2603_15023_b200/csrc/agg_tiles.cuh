@@ -721,6 +721,61 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
   TileCols<STAGED> tc{&p, sm.raw, base, T};
   Misc* misc = sm.misc;
 
+  if (Lcap <= 32) {
+    // ---------------- B2 + B3, at most 32 slots: every warp scans the slot histogram itself
+    // (lane s = slot s, no barrier between B2 and B3); warp w then owns slots w, w + nw, ...
+    // and scans that slot's per-unit counts with lane = unit.
+    const int h = lane < Lcap ? sm.hist[lane] : 0;
+    const int h8 = (h + 7) & ~7, hr = (h + 31) >> 5;
+    int hx = h8, rx = hr;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, hx, d);
+      const int b = __shfl_up_sync(0xffffffffu, rx, d);
+      if (lane >= d) {
+        hx += a;
+        rx += b;
+      }
+    }
+    if (wid == 0 && lane == 31) {
+      misc->nruns = rx;
+      misc->big = 0;
+      misc->nonfinite = 0;
+    }
+    hx -= h8;
+    rx -= hr;
+    for (int s = wid; s < Lcap; s += nw) {
+      const int o0 = __shfl_sync(0xffffffffu, hx, s);
+      const int rb = __shfl_sync(0xffffffffu, rx, s);
+      const int hs = __shfl_sync(0xffffffffu, h, s);
+      int carry = o0;
+      for (int ub = 0; ub < units; ub += 32) {
+        const int u = ub + lane;
+        const int c = u < units ? sm.ucnt[u * Lcap + s] : 0;
+        int inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int a = __shfl_up_sync(0xffffffffu, inc, d);
+          if (lane >= d) inc += a;
+        }
+        if (u < units) sm.ucnt[u * Lcap + s] = (unsigned short)(carry + inc - c);
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      const int q = o0 + hs + lane;  // zero padding rows (mask 0) up to the 8-row boundary
+      if (q < o0 + ((hs + 7) & ~7)) {
+        sm.smask[q] = 0;
+#pragma unroll
+        for (int c = 0; c < NI; ++c) sm.sival[c * TS + q] = 0;
+#pragma unroll
+        for (int c = 0; c < NF; ++c) sm.sfval[c * TS + q] = 0.0;
+        if (MM) sm.smval[q] = 0.0;
+      }
+      for (int i = lane; 32 * i < hs; i += 32) sm.rdesc[rb + i] = pack_run(o0 + 32 * i, s, min(32, hs - 32 * i));
+      if (lane == 0) sm.lrows[s] += (unsigned long long)hs;
+    }
+    __syncthreads();
+    if (tid < Lcap) sm.hist[tid] = 0;  // every warp has read it; the next A1 follows a barrier
+  } else {
   // ---------------- B2: 8-row padded slot offsets and run offsets (one warp)
   if (wid == 0) {
     const int per = (Lcap + 31) / 32;
@@ -756,11 +811,9 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
       misc->nonfinite = 0;
     }
   }
-  // ---------------- B3: unit positions, zero padding rows, run descriptors.  With at most 32
-  // slots, lane s of warp 0 owns slot s in B2 and B3 alike: no barrier in between.
-  const bool b3_warp0 = Lcap <= 32;
-  if (!b3_warp0) __syncthreads();
-  for (int s = b3_warp0 ? (wid == 0 ? lane : Lcap) : tid; s < Lcap; s += b3_warp0 ? 32 : nth) {
+  // ---------------- B3: unit positions, zero padding rows, run descriptors (thread = slot)
+  __syncthreads();
+  for (int s = tid; s < Lcap; s += nth) {
     const int o0 = sm.offs[s];
     int o = o0;
     for (int u = 0; u < units; ++u) {
@@ -782,6 +835,7 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
     sm.hist[s] = 0;  // ready for the next tile's A1
   }
   __syncthreads();
+  }
 
   // ---------------- A2: hash word 0 (two rows per thread, interleaved) + values, written
   // straight to the slot-sorted position; rows still needing flips go to the warp's queue.

@@ -5,6 +5,7 @@
 // order (R12) -- the posterior P makes the release chain inherently sequential
 // (each cell's variance is taken under the posterior left by the previous).
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <new>
 
@@ -44,6 +45,8 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 constexpr int kChainChunk = 16;  // cells per staged chunk of k_finalize_chain
+// chain control block (workspace, 64 B): [0] = first cell of the cell-parallel tail
+constexpr int kCtlTail = 0;
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
                                                        const double* __restrict__ zbuf,
                                                        const uint8_t* __restrict__ is_null, double* P,
                                                        unsigned long long* releases, int jstar, double B,
-                                                       double* release, double* delta_out) {
+                                                       double* release, double* delta_out, long long* ctl) {
   constexpr int H = M / 32;
   constexpr int CH = kChainChunk;
   // cells are streamed through shared memory in chunks of CH (double-buffered cp.async), so
@@ -225,10 +228,18 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
   double p[H];
 #pragma unroll
   for (int h = 0; h < H; ++h) p[h] = P[lane + 32 * h];
+  // exactly one world left in the posterior's support (from then on every cell is R11)
+  auto lone_world = [&]() {
+    int n = 0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) n += __popc(__ballot_sync(0xffffffffu, p[h] > 0.0));
+    return n == 1;
+  };
   unsigned long long nrel = 0;
   const int jl = jstar & 31, jh = jstar >> 5;
-  if (nchunks > 0) stage(0);
-  for (int64_t cell = 0; cell < cells; ++cell) {
+  int64_t tail = lone_world() ? 0 : cells;  // first cell left to k_finalize_tail
+  if (tail > 0 && nchunks > 0) stage(0);
+  for (int64_t cell = 0; cell < tail; ++cell) {
     const int ci = (int)(cell % CH);
     const int b = (int)((cell / CH) & 1);
     if (ci == 0) {
@@ -251,25 +262,35 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
       }
       continue;
     }
-    // pass 1: R11 zero-variance test, the P-mass and the P-weighted sum
-    double llo = INFINITY, lhi = -INFINITY, lsp = 0.0, lspy = 0.0, yjl = 0.0;
+    // pass 1: the P-mass and the P-weighted sum; R11 zero-variance test as the oracle states it:
+    // every y_j with P_j > 0 equals y of the first such world (a NaN there is unequal)
+    double lsp = 0.0, lspy = 0.0, yjl = 0.0;
+    int first = -1;
 #pragma unroll
     for (int h = 0; h < H; ++h) {
-      llo = fmin(llo, p[h] > 0.0 ? y[h] : INFINITY);
-      lhi = fmax(lhi, p[h] > 0.0 ? y[h] : -INFINITY);
       lsp += p[h];
       lspy += __dmul_rn(p[h], y[h]);
       if (h == jh) yjl = y[h];
+      const unsigned bal = __ballot_sync(0xffffffffu, p[h] > 0.0);
+      if (first < 0 && bal) first = 32 * h + __ffs(bal) - 1;
     }
+    double y0 = 0.0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const double t = __shfl_sync(0xffffffffu, y[h], first & 31);
+      if (h == (first >> 5)) y0 = t;
+    }
+    bool eq = true;
+#pragma unroll
+    for (int h = 0; h < H; ++h) eq &= !(p[h] > 0.0) || lane + 32 * h == first || y[h] == y0;
+    const bool all_equal = __all_sync(0xffffffffu, eq);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
-      llo = fmin(llo, __shfl_xor_sync(0xffffffffu, llo, d));
-      lhi = fmax(lhi, __shfl_xor_sync(0xffffffffu, lhi, d));
       lsp += __shfl_xor_sync(0xffffffffu, lsp, d);
       lspy += __shfl_xor_sync(0xffffffffu, lspy, d);
     }
     const double yj = __shfl_sync(0xffffffffu, yjl, jl);
-    if (llo == lhi) {
+    if (all_equal) {
       if (lane == 0) {
         release[cell] = yj;
         if (delta_out) delta_out[cell] = 0.0;
@@ -311,7 +332,11 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
       release[cell] = yt;
       if (delta_out) delta_out[cell] = delta;
     }
+    // R11 makes every later non-NULL cell a zero-variance release once one world is left
+    if (lone_world()) tail = cell + 1;
   }
+  cp_async_wait<0>();
+  if (lane == 0) ctl[kCtlTail] = tail;
   const double tot = warp_sum([&] {
     double t = 0.0;
 #pragma unroll
@@ -323,6 +348,24 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
   if (lane == 0) *releases += nrel;
 }
 
+// The chain after the posterior's support has shrunk to one world (P_w = 1): every NULL cell
+// is NaN, every other cell is a zero-variance release of y_{j*} (R11: with one world there is
+// nothing to compare), and P no longer changes -- so the rest of the chain is cell-parallel.
+template <int M>
+__global__ void k_finalize_tail(const int64_t* num_groups, int64_t G_cap, int A, const double* __restrict__ ybuf,
+                                const uint8_t* __restrict__ is_null, int jstar, double* release, double* delta_out,
+                                const long long* ctl) {
+  const int64_t G = num_groups ? min(*num_groups, G_cap) : G_cap;
+  const int64_t cells = G * A;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t cell = ctl[kCtlTail] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < cells;
+       cell += stride) {
+    const bool null = is_null[cell] != 0;
+    release[cell] = null ? NAN : ybuf[cell * M + jstar];
+    if (delta_out) delta_out[cell] = null ? NAN : 0.0;
+  }
+}
+
 __global__ void __launch_bounds__(32) k_posterior_update(double* P, const double* y, double yt, double delta) {
   const int lane = threadIdx.x;
   double p[2] = {P[lane], P[lane + 32]};
@@ -332,13 +375,29 @@ __global__ void __launch_bounds__(32) k_posterior_update(double* P, const double
   P[lane + 32] = p[1];
 }
 
-static size_t fin_ws(int64_t G_cap, int A, size_t* o_z, size_t* o_n, int M = kM) {
+// workspace: y-vectors [cells][M], normals [cells], chain control block (64 B)
+static size_t fin_ws(int64_t G_cap, int A, size_t* o_z, size_t* o_c, int M = kM) {
   const size_t cells = (size_t)G_cap * A;
   size_t y = cells * M * 8;
   *o_z = (y + 255) & ~(size_t)255;
   size_t z = cells * 8;
-  *o_n = (*o_z + z + 255) & ~(size_t)255;
-  return *o_n + cells + 256;
+  *o_c = (*o_z + z + 255) & ~(size_t)255;
+  return *o_c + 64;
+}
+
+// the release chain: the sequential part, then the cell-parallel tail (empty unless the
+// posterior's support shrank to one world)
+template <int M>
+static void launch_chain(const int64_t* num_groups, int64_t G_cap, int A, const double* ybuf, const double* zbuf,
+                         const uint8_t* is_null, pac_session* s, double* release, double* delta_out, long long* ctl,
+                         cudaStream_t st) {
+  k_finalize_chain<M><<<1, 32, 0, st>>>(num_groups, G_cap, A, ybuf, zbuf, is_null, s->d_P, s->d_count, s->jstar,
+                                        s->B, release, delta_out, ctl);
+  note_launch();
+  const int64_t cells = G_cap * A;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((cells + 255) / 256, 148 * 8));
+  k_finalize_tail<M><<<blocks, 256, 0, st>>>(num_groups, G_cap, A, ybuf, is_null, s->jstar, release, delta_out, ctl);
+  note_launch();
 }
 
 uint64_t session_seed(const pac_session* s) { return s->seed; }
@@ -435,8 +494,8 @@ extern "C" int pac_finalize(pac_session* s, const pac_table* t, const pac_agg_sp
   if (need_count && !t->d_count) return PAC_E_INVAL;
   const int M = t->m ? t->m : 64;
   if (M != s->m) return PAC_E_INVAL;  // the table and the session must agree on m (R29)
-  size_t oz, on;
-  const size_t need = fin_ws(G_cap, n_aggs, &oz, &on, M);
+  size_t oz, oc;
+  const size_t need = fin_ws(G_cap, n_aggs, &oz, &oc, M);
   if (!d_ws || ws_bytes < need) return PAC_E_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)d_ws;
@@ -459,18 +518,16 @@ extern "C" int pac_finalize(pac_session* s, const pac_table* t, const pac_agg_sp
   f.flags = d_flags;
   const int64_t cells = G_cap * n_aggs;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((cells + 7) / 8, 148 * 32));
+  long long* ctl = (long long*)(ws + oc);
   if (M == 64) {
     k_finalize_prep<64><<<blocks, 256, 0, st>>>(f);
     note_launch();
-    k_finalize_chain<64><<<1, 32, 0, st>>>(t->d_num_groups, G_cap, n_aggs, f.ybuf, f.zbuf, d_is_null, s->d_P,
-                                           s->d_count, s->jstar, s->B, d_release, d_delta);
+    launch_chain<64>(t->d_num_groups, G_cap, n_aggs, f.ybuf, f.zbuf, d_is_null, s, d_release, d_delta, ctl, st);
   } else {
     k_finalize_prep<128><<<blocks, 256, 0, st>>>(f);
     note_launch();
-    k_finalize_chain<128><<<1, 32, 0, st>>>(t->d_num_groups, G_cap, n_aggs, f.ybuf, f.zbuf, d_is_null, s->d_P,
-                                            s->d_count, s->jstar, s->B, d_release, d_delta);
+    launch_chain<128>(t->d_num_groups, G_cap, n_aggs, f.ybuf, f.zbuf, d_is_null, s, d_release, d_delta, ctl, st);
   }
-  note_launch();
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
 
@@ -496,8 +553,8 @@ extern "C" int pac_noised_y(pac_session* s, const double* d_y, const uint64_t* d
   if (!s || s->m != 64 || n < 0 || (n > 0 && (!d_y || !d_presence || !d_release || !d_is_null)))
     return PAC_E_INVAL;
   if (n == 0) return PAC_OK;
-  size_t oz, on;
-  const size_t need = fin_ws(n, 1, &oz, &on);
+  size_t oz, oc;
+  const size_t need = fin_ws(n, 1, &oz, &oc);
   if (!d_ws || ws_bytes < need) return PAC_E_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)d_ws;
@@ -506,8 +563,6 @@ extern "C" int pac_noised_y(pac_session* s, const double* d_y, const uint64_t* d
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, 148 * 32));
   k_noised_prep_y<<<blocks, 256, 0, st>>>(d_y, d_presence, n, s->seed, round, ybuf, zbuf, d_is_null);
   note_launch();
-  k_finalize_chain<64><<<1, 32, 0, st>>>(nullptr, n, 1, ybuf, zbuf, d_is_null, s->d_P, s->d_count, s->jstar,
-                                         s->B, d_release, d_delta);
-  note_launch();
+  launch_chain<64>(nullptr, n, 1, ybuf, zbuf, d_is_null, s, d_release, d_delta, (long long*)(ws + oc), st);
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }

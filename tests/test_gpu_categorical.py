@@ -223,3 +223,29 @@ def test_ratio_noised_once_beats_twice_on_gpu(orc):
         once.append(abs(float(rel[0]) - exact) / exact)
         twice.append(abs(float(rel2[0, 0]) / float(rel2[0, 1]) - exact) / exact)
     assert len(once) > 30 and np.mean(once) < np.mean(twice)
+
+
+def test_noised_chain_far_offsets_and_absent_secret_world(orc):
+    """The release chain's variance: large offsets with a small spread (shifted one-pass about
+    y_{j*}), the secret world absent (y_{j*} = 0 far from the mean: the two-pass branch), and
+    single-outlier cells, chained over 3000 releases against the oracle's two-pass (R8, R16)."""
+    seed = 4242
+    jstar, _, P = orc.session(seed)
+    s = pac.Session(seed)
+    rng = np.random.default_rng(8)
+    n = 3000
+    kind = np.arange(n) % 3
+    y = 1e12 + rng.standard_normal((n, 64)) * 1e3
+    y[kind == 2] = rng.integers(0, 100, (int((kind == 2).sum()), 64)).astype(np.float64)
+    y[kind == 2, 5] = 1e9  # one outlier world
+    pres = rng.integers(-(2**63), 2**63 - 1, n, dtype=np.int64).astype(np.uint64)
+    pres |= np.uint64(0xFFFF_FFFF_FFFF_0000)  # mostly present (NULL rate ~ (64 - pc) / 64)
+    bit = np.uint64(1) << np.uint64(jstar)
+    pres[kind == 1] &= ~bit  # y_{j*} reads 0 (R9) while the other worlds sit near 1e12
+    pres[kind != 1] |= bit
+    yo = np.where(((pres[:, None] >> np.arange(64, dtype=np.uint64)) & np.uint64(1)) == 1, y, 0.0)
+    rel, isn, delta = pac.noised_y(s, to_dev(np.ascontiguousarray(y)), _dev_u64(pres))
+    r_o, n_o, d_o, P_o = orc.noised_y(seed, 1 / 128, jstar, P, yo, pres)
+    assert_releases_close(rel.cpu().numpy(), r_o, d_o, isn.cpu().numpy(), n_o)
+    np.testing.assert_allclose(delta.cpu().numpy()[n_o == 0], d_o[n_o == 0], rtol=1e-9, atol=0)
+    np.testing.assert_allclose(s.query()["P"], P_o, rtol=0, atol=1e-9)
