@@ -231,29 +231,6 @@ __device__ __forceinline__ uint64_t row_group_key(const AggPlan& p, int64_t r) {
   return packed;
 }
 
-// Direct HBM update for a row whose group has no CTA-local slot.
-template <int NI, int NF, int MM>
-__device__ __forceinline__ void global_row_update(const AggPlan& p, int prov, uint64_t m,
-                                                  const long long (&iv)[NI > 0 ? NI : 1],
-                                                  const double (&fv)[NF > 0 ? NF : 1], double mv) {
-  atomicAdd(&p.dbg[0], 1ull);
-  if (prov < 0) return;
-  atomicAdd(&p.prov_rows[prov], 1ull);
-  const size_t b = (size_t)prov * kM;
-#pragma unroll 1
-  for (int j = 0; j < kM; ++j) {
-    if (!((m >> j) & 1ull)) continue;
-    atomicAdd(&p.prov_count[b + j], 1ull);
-#pragma unroll
-    for (int c = 0; c < NI; ++c) atomicAdd(&p.prov_isum[c][b + j], (unsigned long long)iv[c]);
-#pragma unroll
-    for (int c = 0; c < NF; ++c) atomicAdd(&p.prov_fsum[c][b + j], fv[c]);
-    if (MM & 1) atomicMin(&p.prov_min[b + j], enc_f64(mv));
-    if (MM & 2) atomicMax(&p.prov_max[b + j], enc_f64(mv));
-  }
-}
-
-// ------------------------------------------------------------------ TMA bulk staging
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -660,6 +637,7 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
     // updates of a row are coalesced device atomics on consecutive addresses
     unsigned gp = __ballot_sync(0xffffffffu, gprov != kNoProv);
     if (gp) {
+      if (lane == 0) atomicAdd(&p.dbg[0], (unsigned long long)__popc(gp));
       uint64_t gm = 0;
       if (gprov != kNoProv) gm = p.mask_in ? tc.w8(0, li) : pac_hash_dev(tc.w8(0, li), p.salt);
       while (gp) {
@@ -668,7 +646,6 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
         const int prov = __shfl_sync(0xffffffffu, gprov, src);
         const uint64_t m = __shfl_sync(0xffffffffu, gm, src);
         const int lsrc = (li & ~31) + src;
-        if (lane == 0) atomicAdd(&p.dbg[0], 1ull);
         if (prov < 0) continue;  // capacity exhausted: reported by the finish kernel
         if (lane == 0) atomicAdd(&p.prov_rows[prov], 1ull);
         const size_t b = (size_t)prov * kM;
