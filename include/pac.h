@@ -137,8 +137,19 @@ typedef struct {
                  d_count / d_world are [G_cap][128]) */
 } pac_table;
 
-/* Workspace bytes for pac_agg_grouped with these aggregates and capacity. */
+/* Workspace bytes for pac_agg_grouped with these aggregates and capacity (the minimum: rows
+ * of groups without a CTA-local slot are then applied with device atomics). */
 int pac_agg_workspace_size(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, size_t* bytes);
+
+/* Workspace bytes for pac_agg_grouped over n_rows rows with the deferred HBM tier: rows of
+ * groups that miss a CTA-local slot (high-cardinality tables, e.g. BASELINE C3) are recorded
+ * (20 B + 8 B per value column each) and folded per group after the pass instead of taking 64
+ * device atomics each.  Equal to pac_agg_workspace_size when no row can miss (G_cap within
+ * the local slot capacity, or MIN/MAX-only aggregates).  pac_agg_grouped uses whatever room
+ * beyond the minimum ws_bytes offers (capacity ~ (ws_bytes - minimum) / record size rows);
+ * rows beyond the capacity fall back to atomics, results identical.  Queries the device. */
+int pac_agg_workspace_size_rows(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, int64_t n_rows,
+                                size_t* bytes);
 
 /* Single-pass 64-world grouped aggregation (§5; PacCountUpdate P:L2254-2258
  * read with ">> j", R4).  For every row r with mask h_r != 0 in group g, and every

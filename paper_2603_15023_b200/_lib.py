@@ -75,6 +75,7 @@ def lib() -> ctypes.CDLL:
         "pac_session_posterior_device": (_P, [_P]),
         "pac_mask": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_uint64, _P, _P]),
         "pac_agg_workspace_size": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int64, _P]),
+        "pac_agg_workspace_size_rows": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _P]),
         "pac_agg_grouped": (ctypes.c_int, [_P, _P, ctypes.c_uint64, _P, ctypes.c_int, _P, ctypes.c_int,
                                            ctypes.c_int64, _P, ctypes.c_int64, _P, ctypes.c_size_t, _P]),
         "pac_table_check": (ctypes.c_int, [_P, _P, _P]),
@@ -120,7 +121,7 @@ def check(fn: str, rc: int) -> None:
 def exported_symbols() -> list:
     return ["pac_session_create", "pac_session_create_m", "pac_session_worlds", "pac_mask128",
             "pac_agg_workspace_size128", "pac_agg_grouped128", "pac_session_destroy", "pac_session_query", "pac_session_set_posterior",
-            "pac_session_posterior_device", "pac_mask", "pac_agg_workspace_size", "pac_agg_grouped",
+            "pac_session_posterior_device", "pac_mask", "pac_agg_workspace_size", "pac_agg_workspace_size_rows", "pac_agg_grouped",
             "pac_table_check", "pac_table_rederive_presence", "pac_table_remap",
             "pac_finalize_workspace_size", "pac_finalize", "pac_posterior_update", "pac_world_vector",
             "pac_lift", "pac_lift_cmp", "pac_noised_y_workspace_size", "pac_noised_y", "pac_cmp_index",

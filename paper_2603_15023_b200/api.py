@@ -196,17 +196,21 @@ def _key_cols(keys: Sequence[torch.Tensor]):
 class Aggregator:
     """pac_agg_grouped with a cached workspace and output table (reused across calls)."""
 
-    def __init__(self, kinds: Sequence[int], G_cap: int, device="cuda"):
+    def __init__(self, kinds: Sequence[int], G_cap: int, device="cuda", spill_rows: Optional[int] = None):
+        """spill_rows: record capacity of the deferred HBM tier (default: every row of the call;
+        0: direct atomics; fewer than the tier rows: the rest take atomics)."""
         self.kinds = list(kinds)
         self.G_cap = int(G_cap)
         self.device = torch.device(device)
         self.table = PacTable.allocate(self.kinds, self.G_cap, self.device)
+        self.spill_rows = spill_rows
         self._ws = None
 
-    def _workspace(self, specs, n_aggs):
+    def _workspace(self, specs, n_aggs, n_rows):
         nb = ctypes.c_size_t()
-        check("pac_agg_workspace_size", L.lib().pac_agg_workspace_size(specs, n_aggs, self.G_cap,
-                                                                         ctypes.byref(nb)))
+        rows = n_rows if self.spill_rows is None else min(n_rows, int(self.spill_rows))
+        check("pac_agg_workspace_size_rows", L.lib().pac_agg_workspace_size_rows(
+            specs, n_aggs, self.G_cap, rows, ctypes.byref(nb)))
         if self._ws is None or self._ws.numel() < nb.value:
             self._ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=self.device)
         return self._ws, nb.value
@@ -221,7 +225,7 @@ class Aggregator:
         kc = _key_cols(keys)
         _require_cuda(pu_key, mask)
         n = (pu_key if pu_key is not None else mask).numel()
-        ws, nb = self._workspace(specs, len(aggs))
+        ws, nb = self._workspace(specs, len(aggs), n)
         t = self.table
         check("pac_agg_grouped", L.lib().pac_agg_grouped(
             _ptr(pu_key), _ptr(mask), salt & 0xFFFFFFFFFFFFFFFF, kc, len(keys), specs, len(aggs), n,

@@ -213,6 +213,173 @@ __global__ void __launch_bounds__(kThreads, PAC_MM_MINB) k_agg_minmax(AggPlan p,
     if (lprov[s] >= 0 && lrows[s]) atomicAdd(&p.prov_rows[lprov[s]], (unsigned long long)lrows[s]);
 }
 
+// ------------------------------------------------------------------ deferred HBM tier
+// Rows of groups without a CTA-local slot were appended to the spill records by tile_a1
+// (AggPlan::sp_*; the pu key is hashed here, by full warps, not in the divergent tier branch).  Instead of 64 device atomics per row on a table far larger than L2, the
+// records are grouped by provisional slot (a counting sort: per-slot counts, slot offsets,
+// scatter of (slot, record) pairs) and each warp then folds a chunk of consecutive pairs in
+// registers, lane j holding worlds j and j+32, with one coalesced atomic flush per slot run.
+
+// per-slot offsets of the grouped order (segments in arbitrary order, one atomic per block);
+// the slot's row count joins prov_rows
+__global__ void __launch_bounds__(256) k_spill_offsets(const int* gcounter, int64_t G_cap, const int* sp_cnt,
+                                                       int* sp_off, unsigned long long* prov_rows,
+                                                       unsigned long long* sp_tot) {
+  __shared__ int wsum[8];
+  __shared__ unsigned long long base;
+  const int64_t G = min((int64_t)*gcounter, G_cap);
+  const int64_t prov = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c = prov < G ? sp_cnt[prov] : 0;
+  int x = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) {
+      const int v = wsum[w];
+      wsum[w] = t;
+      t += v;
+    }
+    base = t ? atomicAdd(sp_tot, (unsigned long long)t) : 0ull;
+  }
+  __syncthreads();
+  if (c) {
+    sp_off[prov] = (int)(base + wsum[wid] + x - c);
+    prov_rows[prov] += (unsigned long long)c;
+  }
+}
+
+// (slot, record) pairs into the slot's segment; lanes of one warp with the same slot share one
+// atomic on the segment cursor
+__global__ void __launch_bounds__(256) k_spill_scatter(const unsigned long long* sp_n, int64_t cap,
+                                                       const int* sp_prov, int* sp_off, int2* pairs) {
+  const int64_t n = min((int64_t)*sp_n, cap);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+    const int64_t i = i0 + threadIdx.x;
+    const int prov = i < n ? sp_prov[i] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, prov >= 0 ? (unsigned)prov : 0x80000000u | lane);
+    const int leader = __ffs(peers) - 1;
+    int b = 0;
+    if (prov >= 0 && lane == leader) b = atomicAdd(&sp_off[prov], __popc(peers));
+    b = __shfl_sync(0xffffffffu, b, leader);
+    if (prov >= 0) pairs[b + __popc(peers & ((1u << lane) - 1u))] = make_int2(prov, (int)i);
+  }
+}
+
+constexpr int kSpillChunk = 256;  // grouped records per warp work item
+
+__device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int src) {
+  const unsigned lo = __shfl_sync(0xffffffffu, (unsigned)v, src);
+  const unsigned hi = __shfl_sync(0xffffffffu, (unsigned)(v >> 32), src);
+  return (unsigned long long)lo | ((unsigned long long)hi << 32);
+}
+
+template <int NI, int NF, int MM>
+__global__ void __launch_bounds__(256) k_spill_agg(AggPlan p, const unsigned long long* sp_tot,
+                                                   const int2* __restrict__ pairs) {
+  const int64_t R = (int64_t)*sp_tot;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t nchunks = (R + kSpillChunk - 1) / kSpillChunk;
+  constexpr int KF = NI, KM = NI + NF;  // value columns: NI int64, NF f64, then the MIN/MAX column
+  for (int64_t ch = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nwarps) {
+    const int64_t c0 = ch * kSpillChunk, c1 = min(R, c0 + kSpillChunk);
+    int cur = -1;
+    unsigned n0 = 0, n1 = 0;
+    long long s0[NI > 0 ? NI : 1], s1[NI > 0 ? NI : 1];
+    double f0[NF > 0 ? NF : 1], f1[NF > 0 ? NF : 1];
+    long long mn0 = kEncPosInf, mn1 = kEncPosInf, mx0 = kEncNegInf, mx1 = kEncNegInf;
+    auto reset = [&]() {
+      n0 = n1 = 0;
+#pragma unroll
+      for (int c = 0; c < NI; ++c) s0[c] = s1[c] = 0;
+#pragma unroll
+      for (int c = 0; c < NF; ++c) f0[c] = f1[c] = 0.0;
+      mn0 = mn1 = kEncPosInf;
+      mx0 = mx1 = kEncNegInf;
+    };
+    auto flush = [&]() {
+      if (cur < 0) return;
+      const size_t b = (size_t)cur * kM;
+      if (p.has_count) {
+        if (n0) atomicAdd(&p.prov_count[b + lane], (unsigned long long)n0);
+        if (n1) atomicAdd(&p.prov_count[b + lane + 32], (unsigned long long)n1);
+      }
+#pragma unroll
+      for (int c = 0; c < NI; ++c) {
+        if (s0[c]) atomicAdd(&p.prov_isum[c][b + lane], (unsigned long long)s0[c]);
+        if (s1[c]) atomicAdd(&p.prov_isum[c][b + lane + 32], (unsigned long long)s1[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < NF; ++c) {
+        if (n0) atomicAdd(&p.prov_fsum[c][b + lane], f0[c]);
+        if (n1) atomicAdd(&p.prov_fsum[c][b + lane + 32], f1[c]);
+      }
+      if ((MM & 1) && mn0 != kEncPosInf) atomicMin(&p.prov_min[b + lane], mn0);
+      if ((MM & 1) && mn1 != kEncPosInf) atomicMin(&p.prov_min[b + lane + 32], mn1);
+      if ((MM & 2) && mx0 != kEncNegInf) atomicMax(&p.prov_max[b + lane], mx0);
+      if ((MM & 2) && mx1 != kEncNegInf) atomicMax(&p.prov_max[b + lane + 32], mx1);
+    };
+    reset();
+    for (int64_t b = c0; b < c1; b += 32) {
+      const int64_t k = b + lane;
+      const int2 pr = k < c1 ? pairs[k] : make_int2(-1, 0);
+      unsigned long long m = 0, v[NI + NF + (MM ? 1 : 0) > 0 ? NI + NF + (MM ? 1 : 0) : 1];
+      if (k < c1) {
+        const unsigned long long r = p.sp_key[pr.y];
+        m = p.mask_in ? r : pac_hash_dev(r, p.salt);
+#pragma unroll
+        for (int c = 0; c < NI + NF + (MM ? 1 : 0); ++c) v[c] = p.sp_val[(size_t)c * p.sp_cap + pr.y];
+      }
+      const int nb = (int)min((int64_t)32, c1 - b);
+      for (int t = 0; t < nb; ++t) {
+        const int prov = __shfl_sync(0xffffffffu, pr.x, t);
+        if (prov != cur) {
+          flush();
+          reset();
+          cur = prov;
+        }
+        const unsigned long long mt = shfl_u64(m, t);
+        const bool w0 = (mt >> lane) & 1ull, w1 = (mt >> (lane + 32)) & 1ull;
+        n0 += w0;
+        n1 += w1;
+#pragma unroll
+        for (int c = 0; c < NI; ++c) {
+          const long long x = (long long)shfl_u64(v[c], t);
+          s0[c] += w0 ? x : 0;
+          s1[c] += w1 ? x : 0;
+        }
+#pragma unroll
+        for (int c = 0; c < NF; ++c) {
+          const double x = __longlong_as_double((long long)shfl_u64(v[KF + c], t));
+          if (w0) f0[c] += x;
+          if (w1) f1[c] += x;
+        }
+        if (MM) {
+          const long long e = enc_f64(__longlong_as_double((long long)shfl_u64(v[KM], t)));
+          if (w0) {
+            mn0 = min(mn0, e);
+            mx0 = max(mx0, e);
+          }
+          if (w1) {
+            mn1 = min(mn1, e);
+            mx1 = max(mx1, e);
+          }
+        }
+      }
+    }
+    flush();
+  }
+}
+
 // ------------------------------------------------------------------ finish: count, sort, gather
 __global__ void k_finish_count(AggPlan p, int n_keys, int64_t* num_groups, int* status,
                                int* Gdev) {
@@ -488,7 +655,7 @@ static WsLayout ws_layout(const AccSet& A, int64_t G_cap) {
   w.Hcap = next_pow2(std::max<int64_t>(2 * Gc, 64));
   w.o_gkey = take(8 * w.Hcap);
   w.o_gstate = take(4 * w.Hcap);
-  w.o_ctr = take(64);  // gcounter, Gdev, gmaxabs
+  w.o_ctr = take(64);  // gcounter, Gdev, gmaxabs, dbg[2], spill records reserved, spill records grouped
   w.o_pkey = take(8 * Gc);
   w.o_prows = take(8 * Gc);
   w.o_pcount = A.has_count ? take(8 * Gc * kM) : 0;
@@ -508,6 +675,45 @@ static WsLayout ws_layout(const AccSet& A, int64_t G_cap) {
   w.o_meta = take(2 * PAC_MAX_AGGS * 4);
   w.bytes = off;
   return w;
+}
+
+// Deferred HBM tier records, appended after the base layout: per-slot counts and offsets,
+// then cap records (slot 4 B, mask 8 B, 8 B per value column) and cap (slot, record) pairs.
+struct SpillLayout {
+  size_t o_cnt, o_off, o_prov, o_mask, o_val, o_pairs, bytes;
+  int64_t cap;
+};
+
+static int spill_values(const AccSet& A) { return A.ni + A.nf + ((A.has_min || A.has_max) ? 1 : 0); }
+
+static SpillLayout spill_layout(const AccSet& A, int64_t G_cap, size_t base, int64_t cap) {
+  SpillLayout s{};
+  size_t off = base;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const int64_t Gc = G_cap < 1 ? 1 : G_cap;
+  s.cap = cap;
+  s.o_cnt = take(4 * Gc);
+  s.o_off = take(4 * Gc);
+  s.o_prov = take(4 * cap);
+  s.o_mask = take(8 * cap);
+  s.o_val = take(8 * (size_t)spill_values(A) * cap);
+  s.o_pairs = take(8 * cap);
+  s.bytes = off;
+  return s;
+}
+
+// the largest record capacity (<= n_rows) the caller's workspace holds beyond the base layout
+static int64_t spill_fit(const AccSet& A, int64_t G_cap, size_t base, size_t ws_bytes, int64_t n_rows) {
+  const size_t fixed = spill_layout(A, G_cap, base, 0).bytes + 4 * 256;
+  if (ws_bytes <= fixed) return 0;
+  const size_t rec = 20 + 8 * (size_t)spill_values(A);
+  int64_t cap = std::min<int64_t>((int64_t)((ws_bytes - fixed) / rec), std::min<int64_t>(n_rows, INT32_MAX - 1));
+  while (cap > 0 && spill_layout(A, G_cap, base, cap).bytes > ws_bytes) cap -= 1024;
+  return cap < 1024 ? 0 : cap;
 }
 
 static int raw_tile_bytes(const AccSet& A, int T, int key_bytes) {
@@ -704,6 +910,19 @@ static const LaunchFn kLaunchTm[3][3][4] = {
     {PAC_TMM_ROW(2, 0), PAC_TMM_ROW(2, 1), PAC_TMM_ROW(2, 2)},
 };
 
+typedef void (*SpillFn)(const AggPlan&, const unsigned long long*, const int2*, int, cudaStream_t);
+template <int NI, int NF, int MM>
+static void launch_spill(const AggPlan& p, const unsigned long long* tot, const int2* pairs, int grid,
+                         cudaStream_t st) {
+  k_spill_agg<NI, NF, MM><<<grid, 256, 0, st>>>(p, tot, pairs);
+}
+#define PAC_SP_ROW(NI, NF) {launch_spill<NI, NF, 0>, launch_spill<NI, NF, 1>, launch_spill<NI, NF, 2>, launch_spill<NI, NF, 3>}
+static const SpillFn kSpill[3][3][4] = {
+    {PAC_SP_ROW(0, 0), PAC_SP_ROW(0, 1), PAC_SP_ROW(0, 2)},
+    {PAC_SP_ROW(1, 0), PAC_SP_ROW(1, 1), PAC_SP_ROW(1, 2)},
+    {PAC_SP_ROW(2, 0), PAC_SP_ROW(2, 1), PAC_SP_ROW(2, 2)},
+};
+
 static int device_info(int* sms, int* smem_optin) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return PAC_E_CUDA;
@@ -742,6 +961,24 @@ extern "C" int pac_agg_workspace_size(const pac_agg_spec* aggs, int n_aggs, int6
   int rc = build_accs(aggs, n_aggs, &A, true);
   if (rc) return rc;
   *bytes = ws_layout(A, G_cap).bytes;
+  return PAC_OK;
+}
+
+extern "C" int pac_agg_workspace_size_rows(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, int64_t n_rows,
+                                           size_t* bytes) {
+  if (!bytes || G_cap < 1 || n_rows < 0) return PAC_E_INVAL;
+  AccSet A;
+  int rc = build_accs(aggs, n_aggs, &A, true);
+  if (rc) return rc;
+  const size_t base = ws_layout(A, G_cap).bytes;
+  *bytes = base;
+  if (!A.has_count || n_rows == 0) return PAC_OK;  // MIN/MAX-only: k_agg_minmax, no deferred tier
+  int sms = 148, smem_max = 0;
+  if (device_info(&sms, &smem_max) != PAC_OK) return PAC_E_CUDA;
+  SmemLayout L{};
+  if (!choose_layout(A, G_cap, smem_max, 8, &L)) return PAC_E_INVAL;
+  if (G_cap <= L.Lcap) return PAC_OK;  // every group can hold a CTA-local slot: no tier rows
+  *bytes = spill_layout(A, G_cap, base, std::min<int64_t>(n_rows, INT32_MAX - 1)).bytes + 4 * 256;
   return PAC_OK;
 }
 
@@ -874,9 +1111,35 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
                 L.tm ? "_tm" : "", A.ni, A.nf, (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0), L.T, L.Lcap, L.LH, L.bytes,
                 (long long)G_cap);
       const int mm = (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0);
+      // deferred HBM tier when groups can miss a CTA-local slot and the workspace has room
+      SpillLayout S{};
+      if (G_cap > L.Lcap && !getenv("PAC_NO_SPILL")) {
+        const int64_t cap = spill_fit(A, G_cap, W.bytes, ws_bytes, n_rows);
+        if (cap > 0) S = spill_layout(A, G_cap, W.bytes, cap);
+      }
+      if (S.cap > 0) {
+        p.sp_cap = S.cap;
+        p.sp_n = (unsigned long long*)(ws + W.o_ctr + 32);
+        p.sp_prov = (int*)(ws + S.o_prov);
+        p.sp_key = (unsigned long long*)(ws + S.o_mask);
+        p.sp_val = (unsigned long long*)(ws + S.o_val);
+        p.sp_cnt = (int*)(ws + S.o_cnt);
+        if (cudaMemsetAsync(p.sp_cnt, 0, 4 * (size_t)G_cap, st) != cudaSuccess) return PAC_E_CUDA;
+      }
       profile_begin(st);
       e = L.tm ? kLaunchTm[A.ni][A.nf][mm](p, L, sms, st) : kLaunch[A.ni][A.nf][mm](p, L, sms, st);
       profile_end(st);
+      if (e == cudaSuccess && S.cap > 0) {
+        unsigned long long* sp_tot = (unsigned long long*)(ws + W.o_ctr + 40);
+        int* sp_off = (int*)(ws + S.o_off);
+        int2* pairs = (int2*)(ws + S.o_pairs);
+        k_spill_offsets<<<(int)((G_cap + 255) / 256), 256, 0, st>>>(p.gcounter, G_cap, p.sp_cnt, sp_off,
+                                                                   p.prov_rows, sp_tot);
+        k_spill_scatter<<<sms * 8, 256, 0, st>>>(p.sp_n, S.cap, p.sp_prov, sp_off, pairs);
+        kSpill[A.ni][A.nf][mm](p, sp_tot, pairs, sms * 8, st);
+        for (int q = 0; q < 3; ++q) note_launch();
+        e = cudaGetLastError();
+      }
     }
     if (e != cudaSuccess) return PAC_E_CUDA;
   }

@@ -61,6 +61,16 @@ struct AggPlan {
   double* prov_fsum[2];
   long long* prov_min;
   long long* prov_max;
+  // deferred HBM tier (agg.cu k_spill_*): rows of groups without a CTA-local slot are appended
+  // here (record i: sp_prov[i], sp_key[i] = the pu key, or the mask when mask_in, raw 8-byte
+  // values sp_val[k * sp_cap + i] in column order) and aggregated after the pass, grouped by
+  // slot; sp_cap = 0: direct atomics
+  int64_t sp_cap;
+  unsigned long long* sp_n;  // records reserved (may exceed sp_cap: the excess took atomics)
+  int* sp_prov;
+  unsigned long long* sp_key;
+  unsigned long long* sp_val;
+  int* sp_cnt;  // [G_cap] records per provisional slot
 };
 
 struct SmemLayout {
@@ -135,17 +145,29 @@ __host__ __device__ constexpr SmemLayout tile_layout(int ni, int nf, int has_min
 }
 
 // ------------------------------------------------------------------ dictionaries
+// 64 consecutive 8-byte words = v, as 16-byte stores (one thread; slot rows are 512 B aligned)
+__device__ __forceinline__ void fill_world_row(void* dst, long long v) {
+  longlong2* d = (longlong2*)dst;
+  const longlong2 x = make_longlong2(v, v);
+#pragma unroll 8
+  for (int i = 0; i < kM / 2; ++i) d[i] = x;
+}
+
 __device__ __forceinline__ void init_prov_slot(const AggPlan& p, int prov, uint64_t key) {
   p.prov_key[prov] = key;
   p.prov_rows[prov] = 0;
-  size_t b = (size_t)prov * kM;
-  for (int j = 0; j < kM; ++j) {
-    if (p.has_count) p.prov_count[b + j] = 0;
-    for (int c = 0; c < p.ni; ++c) p.prov_isum[c][b + j] = 0;
-    for (int c = 0; c < p.nf; ++c) p.prov_fsum[c][b + j] = 0.0;
-    if (p.has_min) p.prov_min[b + j] = kEncPosInf;
-    if (p.has_max) p.prov_max[b + j] = kEncNegInf;
-  }
+  const size_t b = (size_t)prov * kM;
+  if (p.has_count) fill_world_row(p.prov_count + b, 0);
+  for (int c = 0; c < p.ni; ++c) fill_world_row(p.prov_isum[c] + b, 0);
+  for (int c = 0; c < p.nf; ++c) fill_world_row(p.prov_fsum[c] + b, 0);  // +0.0
+  if (p.has_min) fill_world_row(p.prov_min + b, kEncPosInf);
+  if (p.has_max) fill_world_row(p.prov_max + b, kEncNegInf);
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* a) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
 }
 
 // Insert-or-find `key` in the HBM dictionary; returns the provisional slot, or -1 when
@@ -153,7 +175,9 @@ __device__ __forceinline__ void init_prov_slot(const AggPlan& p, int prov, uint6
 static __device__ int global_slot(const AggPlan& p, uint64_t key) {
   uint32_t h = dict_hash(key) & p.hmask;
   for (;;) {
-    int st = *(volatile int*)&p.gstate[h];
+    // acquire: a published state orders the key read after it (the writer releases with a
+    // fence before publishing)
+    const int st = ld_acquire_gpu(&p.gstate[h]);
     if (st == 0) {
       if (atomicCAS(&p.gstate[h], 0, -1) == 0) {
         int prov = atomicAdd(p.gcounter, 1);
@@ -171,7 +195,6 @@ static __device__ int global_slot(const AggPlan& p, uint64_t key) {
       continue;
     }
     if (st < 0) continue;  // being written
-    __threadfence();
     if (*(volatile unsigned long long*)&p.gkey[h] == key) return st - 1;
     h = (h + 1) & p.hmask;
   }
@@ -188,6 +211,8 @@ static __device__ int local_code(const AggPlan& p, uint64_t key, unsigned long l
   for (;;) {
     int st = *(volatile int*)&lstate[h];
     if (st == 0) {
+      // a full dictionary stays full: skip the claim-and-release
+      if (*(volatile int*)&misc->ndict >= LH / 2) return kOvfBase + global_slot(p, key) + 1;
       if (atomicCAS(&lstate[h], 0, -1) == 0) {
         if (atomicAdd(&misc->ndict, 1) >= LH / 2) {  // too full: release, use the HBM tier
           atomicSub(&misc->ndict, 1);
@@ -638,8 +663,29 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
     unsigned gp = __ballot_sync(0xffffffffu, gprov != kNoProv);
     if (gp) {
       if (lane == 0) atomicAdd(&p.dbg[0], (unsigned long long)__popc(gp));
+      if (p.sp_cap > 0) {  // deferred: append the warp's tier rows to the spill records
+        const bool mine = gprov != kNoProv && gprov >= 0;
+        const unsigned sb = __ballot_sync(0xffffffffu, mine);
+        unsigned long long b0 = 0;
+        if (lane == 0 && sb) b0 = atomicAdd(p.sp_n, (unsigned long long)__popc(sb));
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        const unsigned long long i = b0 + __popc(sb & lt_mask);
+        if (b0 + __popc(sb) <= (unsigned long long)p.sp_cap) {
+          if (mine) {
+            p.sp_prov[i] = gprov;
+            p.sp_key[i] = tc.w8(0, li);  // hashed by k_spill_agg with full warps
+            unsigned long long* v = p.sp_val + i;
+#pragma unroll
+            for (int c = 0; c < KK - 1; ++c) v[(size_t)c * p.sp_cap] = tc.w8(1 + c, li);
+            atomicAdd(&p.sp_cnt[gprov], 1);
+          }
+          gp = 0;
+        } else if (mine && i < (unsigned long long)p.sp_cap) {
+          p.sp_prov[i] = -1;  // reserved but full: these rows take the atomics below
+        }
+      }
       uint64_t gm = 0;
-      if (gprov != kNoProv) gm = p.mask_in ? tc.w8(0, li) : pac_hash_dev(tc.w8(0, li), p.salt);
+      if (gp && gprov != kNoProv) gm = p.mask_in ? tc.w8(0, li) : pac_hash_dev(tc.w8(0, li), p.salt);
       while (gp) {
         const int src = __ffs(gp) - 1;
         gp &= gp - 1;

@@ -20,9 +20,9 @@ def workload_aggs(w, cols):
     return [(k, None if i < 0 else cols["values"][i]) for k, i in w.aggs]
 
 
-def run_gpu(aggs_host, keys_host, pu=None, masks=None, salt=0, G_cap=1024):
+def run_gpu(aggs_host, keys_host, pu=None, masks=None, salt=0, G_cap=1024, spill_rows=None):
     import paper_2603_15023_b200 as pac
-    ag = pac.Aggregator([k for k, _ in aggs_host], G_cap)
+    ag = pac.Aggregator([k for k, _ in aggs_host], G_cap, spill_rows=spill_rows)
     cache = {}  # one device copy per host column (aggregates may share a column)
     vals = []
     for _, v in aggs_host:
