@@ -143,7 +143,7 @@ int pac_agg_workspace_size(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, 
 
 /* Workspace bytes for pac_agg_grouped over n_rows rows with the deferred HBM tier: rows of
  * groups that miss a CTA-local slot (high-cardinality tables, e.g. BASELINE C3) are recorded
- * (20 B + 8 B per value column each) and folded per group after the pass instead of taking 64
+ * (28 B + 8 B per value column each) and folded per group after the pass instead of taking 64
  * device atomics each.  Equal to pac_agg_workspace_size when no row can miss (G_cap within
  * the local slot capacity, or MIN/MAX-only aggregates).  pac_agg_grouped uses whatever room
  * beyond the minimum ws_bytes offers (capacity ~ (ws_bytes - minimum) / record size rows);

@@ -220,6 +220,25 @@ __global__ void __launch_bounds__(kThreads, PAC_MM_MINB) k_agg_minmax(AggPlan p,
 // scatter of (slot, record) pairs) and each warp then folds a chunk of consecutive pairs in
 // registers, lane j holding worlds j and j+32, with one coalesced atomic flush per slot run.
 
+// HBM slots of the records the CTA dictionaries could not resolve (full warps, high occupancy:
+// the dictionary probes' latency overlaps across warps instead of stalling the tile pipeline),
+// then the per-slot record counts
+__global__ void __launch_bounds__(256) k_spill_resolve(AggPlan p) {
+  const int64_t n = min((int64_t)*p.sp_n, p.sp_cap);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+    const int64_t i = i0 + threadIdx.x;
+    int prov = i < n ? p.sp_prov[i] : -1;
+    if (prov == -2) {
+      prov = global_slot(p, p.sp_gkey[i]);
+      p.sp_prov[i] = prov;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, prov >= 0 ? (unsigned)prov : 0x80000000u | lane);
+    if (prov >= 0 && lane == __ffs(peers) - 1) atomicAdd(&p.sp_cnt[prov], __popc(peers));
+  }
+}
+
 // per-slot offsets of the grouped order (segments in arbitrary order, one atomic per block);
 // the slot's row count joins prov_rows
 __global__ void __launch_bounds__(256) k_spill_offsets(const int* gcounter, int64_t G_cap, const int* sp_cnt,
@@ -680,7 +699,7 @@ static WsLayout ws_layout(const AccSet& A, int64_t G_cap) {
 // Deferred HBM tier records, appended after the base layout: per-slot counts and offsets,
 // then cap records (slot 4 B, mask 8 B, 8 B per value column) and cap (slot, record) pairs.
 struct SpillLayout {
-  size_t o_cnt, o_off, o_prov, o_mask, o_val, o_pairs, bytes;
+  size_t o_cnt, o_off, o_prov, o_gkey, o_mask, o_val, o_pairs, bytes;
   int64_t cap;
 };
 
@@ -699,6 +718,7 @@ static SpillLayout spill_layout(const AccSet& A, int64_t G_cap, size_t base, int
   s.o_cnt = take(4 * Gc);
   s.o_off = take(4 * Gc);
   s.o_prov = take(4 * cap);
+  s.o_gkey = take(8 * cap);
   s.o_mask = take(8 * cap);
   s.o_val = take(8 * (size_t)spill_values(A) * cap);
   s.o_pairs = take(8 * cap);
@@ -710,7 +730,7 @@ static SpillLayout spill_layout(const AccSet& A, int64_t G_cap, size_t base, int
 static int64_t spill_fit(const AccSet& A, int64_t G_cap, size_t base, size_t ws_bytes, int64_t n_rows) {
   const size_t fixed = spill_layout(A, G_cap, base, 0).bytes + 4 * 256;
   if (ws_bytes <= fixed) return 0;
-  const size_t rec = 20 + 8 * (size_t)spill_values(A);
+  const size_t rec = 28 + 8 * (size_t)spill_values(A);
   int64_t cap = std::min<int64_t>((int64_t)((ws_bytes - fixed) / rec), std::min<int64_t>(n_rows, INT32_MAX - 1));
   while (cap > 0 && spill_layout(A, G_cap, base, cap).bytes > ws_bytes) cap -= 1024;
   return cap < 1024 ? 0 : cap;
@@ -1121,6 +1141,7 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
         p.sp_cap = S.cap;
         p.sp_n = (unsigned long long*)(ws + W.o_ctr + 32);
         p.sp_prov = (int*)(ws + S.o_prov);
+        p.sp_gkey = (unsigned long long*)(ws + S.o_gkey);
         p.sp_key = (unsigned long long*)(ws + S.o_mask);
         p.sp_val = (unsigned long long*)(ws + S.o_val);
         p.sp_cnt = (int*)(ws + S.o_cnt);
@@ -1133,11 +1154,12 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
         unsigned long long* sp_tot = (unsigned long long*)(ws + W.o_ctr + 40);
         int* sp_off = (int*)(ws + S.o_off);
         int2* pairs = (int2*)(ws + S.o_pairs);
+        k_spill_resolve<<<sms * 16, 256, 0, st>>>(p);
         k_spill_offsets<<<(int)((G_cap + 255) / 256), 256, 0, st>>>(p.gcounter, G_cap, p.sp_cnt, sp_off,
                                                                    p.prov_rows, sp_tot);
         k_spill_scatter<<<sms * 8, 256, 0, st>>>(p.sp_n, S.cap, p.sp_prov, sp_off, pairs);
         kSpill[A.ni][A.nf][mm](p, sp_tot, pairs, sms * 8, st);
-        for (int q = 0; q < 3; ++q) note_launch();
+        for (int q = 0; q < 4; ++q) note_launch();
         e = cudaGetLastError();
       }
     }

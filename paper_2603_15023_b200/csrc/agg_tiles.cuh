@@ -19,6 +19,7 @@ constexpr int kTileThreads = 256;  // k_agg_tiles
 #define PAC_TILE_MINB 3  // min resident CTAs per SM the register allocation targets
 #endif
 constexpr int kOvfBase = 0x20000000;
+constexpr int kUnresolved = 0x7FFFFFFF;  // local_code(defer): not in the CTA dictionary, HBM slot not looked up
 #ifdef PAC_ABLATE_BUILD
 constexpr bool kAblate = true;   // profiling build: PAC_ABLATE switches phases off
 #else
@@ -62,12 +63,14 @@ struct AggPlan {
   long long* prov_min;
   long long* prov_max;
   // deferred HBM tier (agg.cu k_spill_*): rows of groups without a CTA-local slot are appended
-  // here (record i: sp_prov[i], sp_key[i] = the pu key, or the mask when mask_in, raw 8-byte
-  // values sp_val[k * sp_cap + i] in column order) and aggregated after the pass, grouped by
-  // slot; sp_cap = 0: direct atomics
+  // here (record i: sp_prov[i] = the HBM slot, or -2 when the CTA dictionary did not know it
+  // (resolved from the group key sp_gkey[i] after the pass), sp_key[i] = the pu key, or the
+  // mask when mask_in, raw 8-byte values sp_val[k * sp_cap + i] in column order) and
+  // aggregated after the pass, grouped by slot; sp_cap = 0: direct atomics
   int64_t sp_cap;
   unsigned long long* sp_n;  // records reserved (may exceed sp_cap: the excess took atomics)
   int* sp_prov;
+  unsigned long long* sp_gkey;
   unsigned long long* sp_key;
   unsigned long long* sp_val;
   int* sp_cnt;  // [G_cap] records per provisional slot
@@ -205,20 +208,22 @@ static __device__ int global_slot(const AggPlan& p, uint64_t key) {
 // An empty entry is claimed with CAS first; only then is the entry counted, so concurrent
 // contenders for one key never inflate the fill count.  At half full no more keys are
 // inserted (their rows use the HBM dictionary directly).
+// defer: a key the full dictionary cannot take returns kUnresolved instead of its HBM slot (the
+// deferred tier resolves it after the pass, k_spill_resolve).
 static __device__ int local_code(const AggPlan& p, uint64_t key, unsigned long long* lkey, int* lstate,
-                          int LH, int* lprov, int Lcap, Misc* misc) {
+                          int LH, int* lprov, int Lcap, Misc* misc, bool defer = false) {
   uint32_t h = (((uint32_t)key ^ (uint32_t)(key >> 32)) * 0x9E3779B1u) >> 16 & (LH - 1);
   for (;;) {
     int st = *(volatile int*)&lstate[h];
     if (st == 0) {
       // a full dictionary stays full: skip the claim-and-release
-      if (*(volatile int*)&misc->ndict >= LH / 2) return kOvfBase + global_slot(p, key) + 1;
+      if (*(volatile int*)&misc->ndict >= LH / 2) return defer ? kUnresolved : kOvfBase + global_slot(p, key) + 1;
       if (atomicCAS(&lstate[h], 0, -1) == 0) {
         if (atomicAdd(&misc->ndict, 1) >= LH / 2) {  // too full: release, use the HBM tier
           atomicSub(&misc->ndict, 1);
           __threadfence_block();
           atomicExch(&lstate[h], 0);
-          return kOvfBase + global_slot(p, key) + 1;
+          return defer ? kUnresolved : kOvfBase + global_slot(p, key) + 1;
         }
         lkey[h] = key;
         int s = atomicAdd(&misc->nlocal, 1);
@@ -641,16 +646,21 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
   constexpr int KK = 1 + NI + NF + (MM ? 1 : 0);
   TileCols<STAGED> tc{&p, sm.raw, base, T};
   constexpr int kNoProv = INT_MIN;
+  constexpr int kDeferred = -2;  // HBM slot not looked up yet (deferred tier)
+  const bool defer = p.sp_cap > 0;
   for (int li = tid; li < T; li += nth) {
     int s = -1;
     int gprov = kNoProv;  // provisional HBM slot of a row without a local slot (-1: no capacity)
+    uint64_t key = 0;
     if (li < tn) {
       bool keep = true;
       if (p.mask_in) keep = tc.w8(0, li) != 0ull;  // R21: a row in no world is dropped
       if (keep) {
-        const uint64_t key = tc.group_key(KK, li);
-        const int code = local_code(p, key, sm.lkey, sm.lstate, LH, sm.lprov, Lcap, sm.misc);
-        if (code < kOvfBase) {
+        key = tc.group_key(KK, li);
+        const int code = local_code(p, key, sm.lkey, sm.lstate, LH, sm.lprov, Lcap, sm.misc, defer);
+        if (code == kUnresolved) {
+          gprov = kDeferred;
+        } else if (code < kOvfBase) {
           s = code - 1;
         } else {  // no local slot: the HBM tier, below
           gprov = code - kOvfBase - 1;
@@ -664,7 +674,7 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
     if (gp) {
       if (lane == 0) atomicAdd(&p.dbg[0], (unsigned long long)__popc(gp));
       if (p.sp_cap > 0) {  // deferred: append the warp's tier rows to the spill records
-        const bool mine = gprov != kNoProv && gprov >= 0;
+        const bool mine = gprov != kNoProv && gprov != -1;
         const unsigned sb = __ballot_sync(0xffffffffu, mine);
         unsigned long long b0 = 0;
         if (lane == 0 && sb) b0 = atomicAdd(p.sp_n, (unsigned long long)__popc(sb));
@@ -673,11 +683,11 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
         if (b0 + __popc(sb) <= (unsigned long long)p.sp_cap) {
           if (mine) {
             p.sp_prov[i] = gprov;
+            p.sp_gkey[i] = key;
             p.sp_key[i] = tc.w8(0, li);  // hashed by k_spill_agg with full warps
             unsigned long long* v = p.sp_val + i;
 #pragma unroll
             for (int c = 0; c < KK - 1; ++c) v[(size_t)c * p.sp_cap] = tc.w8(1 + c, li);
-            atomicAdd(&p.sp_cnt[gprov], 1);
           }
           gp = 0;
         } else if (mine && i < (unsigned long long)p.sp_cap) {
@@ -685,6 +695,7 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
         }
       }
       uint64_t gm = 0;
+      if (gp && gprov == kDeferred) gprov = global_slot(p, key);  // records full: resolve now
       if (gp && gprov != kNoProv) gm = p.mask_in ? tc.w8(0, li) : pac_hash_dev(tc.w8(0, li), p.salt);
       while (gp) {
         const int src = __ffs(gp) - 1;
