@@ -726,12 +726,16 @@ static SpillLayout spill_layout(const AccSet& A, int64_t G_cap, size_t base, int
   return s;
 }
 
-// the largest record capacity (<= n_rows) the caller's workspace holds beyond the base layout
+// records for n_rows tier rows: each warp may leave up to one partial grab of kSpillGrab unused
+static int64_t spill_rows_needed(int64_t n_rows) { return n_rows + (int64_t)4096 * kSpillGrab; }
+
+// the largest record capacity the caller's workspace holds beyond the base layout
 static int64_t spill_fit(const AccSet& A, int64_t G_cap, size_t base, size_t ws_bytes, int64_t n_rows) {
   const size_t fixed = spill_layout(A, G_cap, base, 0).bytes + 4 * 256;
   if (ws_bytes <= fixed) return 0;
   const size_t rec = 28 + 8 * (size_t)spill_values(A);
-  int64_t cap = std::min<int64_t>((int64_t)((ws_bytes - fixed) / rec), std::min<int64_t>(n_rows, INT32_MAX - 1));
+  int64_t cap = std::min<int64_t>((int64_t)((ws_bytes - fixed) / rec),
+                                  std::min<int64_t>(spill_rows_needed(n_rows), INT32_MAX - 1));
   while (cap > 0 && spill_layout(A, G_cap, base, cap).bytes > ws_bytes) cap -= 1024;
   return cap < 1024 ? 0 : cap;
 }
@@ -998,7 +1002,7 @@ extern "C" int pac_agg_workspace_size_rows(const pac_agg_spec* aggs, int n_aggs,
   SmemLayout L{};
   if (!choose_layout(A, G_cap, smem_max, 8, &L)) return PAC_E_INVAL;
   if (G_cap <= L.Lcap) return PAC_OK;  // every group can hold a CTA-local slot: no tier rows
-  *bytes = spill_layout(A, G_cap, base, std::min<int64_t>(n_rows, INT32_MAX - 1)).bytes + 4 * 256;
+  *bytes = spill_layout(A, G_cap, base, std::min<int64_t>(spill_rows_needed(n_rows), INT32_MAX - 1)).bytes + 4 * 256;
   return PAC_OK;
 }
 

@@ -633,10 +633,48 @@ struct TileCols {
 // and the run table, so a warp runs its share of C(t) and then its share of A1(t+1) with no
 // barrier in between.
 
+// Per-warp cursor into the deferred-tier records: the warp reserves kSpillGrab records at a time
+// (one device atomic per kSpillGrab tier rows, not per 32) and marks what it leaves unused
+// (slot -1).  ntier counts the warp's tier rows (debug statistic, one atomic per warp).
+constexpr int kSpillGrab = 256;
+struct SpillCur {
+  unsigned long long cur, end;
+  unsigned long long ntier;
+  __device__ __forceinline__ void init() { cur = end = 0; ntier = 0; }
+  // marks [cur, end) unused; every lane of the warp calls it
+  __device__ __forceinline__ void retire(const AggPlan& p, int lane) {
+    for (unsigned long long i = cur + lane; i < end; i += 32) p.sp_prov[i] = -1;
+    cur = end;
+  }
+  // n <= 32 records for the calling warp: base index, or ~0 when the records are full
+  __device__ __forceinline__ unsigned long long take(const AggPlan& p, int n, int lane) {
+    if (cur + n > end) {
+      retire(p, lane);
+      unsigned long long b = 0;
+      if (lane == 0) b = atomicAdd(p.sp_n, (unsigned long long)kSpillGrab);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      const unsigned long long cap = (unsigned long long)p.sp_cap;
+      cur = b < cap ? b : cap;
+      end = b + kSpillGrab < cap ? b + kSpillGrab : cap;
+      if (cur + n > end) {  // the records are full: this and every later row takes atomics
+        retire(p, lane);
+        return ~0ull;
+      }
+    }
+    const unsigned long long b = cur;
+    cur += n;
+    return b;
+  }
+  __device__ __forceinline__ void finish(const AggPlan& p, int lane) {
+    if (p.sp_cap > 0) retire(p, lane);
+    if (lane == 0 && ntier) atomicAdd(&p.dbg[0], ntier);
+  }
+};
+
 // A1: group slot of every row, rank within its 32-row unit, per-unit and per-tile slot counts.
 template <int NI, int NF, int MM, bool STAGED>
 __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, const SmemLayout& L, int64_t base,
-                                        int tn) {
+                                        int tn, SpillCur& sc) {
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31;
   const int T = L.T, Lcap = L.Lcap, LH = L.LH;
   const unsigned short kNone = 0xFFFF;
@@ -672,15 +710,13 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
     // updates of a row are coalesced device atomics on consecutive addresses
     unsigned gp = __ballot_sync(0xffffffffu, gprov != kNoProv);
     if (gp) {
-      if (lane == 0) atomicAdd(&p.dbg[0], (unsigned long long)__popc(gp));
+      sc.ntier += __popc(gp);
       if (p.sp_cap > 0) {  // deferred: append the warp's tier rows to the spill records
         const bool mine = gprov != kNoProv && gprov != -1;
         const unsigned sb = __ballot_sync(0xffffffffu, mine);
-        unsigned long long b0 = 0;
-        if (lane == 0 && sb) b0 = atomicAdd(p.sp_n, (unsigned long long)__popc(sb));
-        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        const unsigned long long b0 = sb ? sc.take(p, __popc(sb), lane) : 0ull;
         const unsigned long long i = b0 + __popc(sb & lt_mask);
-        if (b0 + __popc(sb) <= (unsigned long long)p.sp_cap) {
+        if (b0 != ~0ull) {
           if (mine) {
             p.sp_prov[i] = gprov;
             p.sp_gkey[i] = key;
@@ -690,8 +726,6 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
             for (int c = 0; c < KK - 1; ++c) v[(size_t)c * p.sp_cap] = tc.w8(1 + c, li);
           }
           gp = 0;
-        } else if (mine && i < (unsigned long long)p.sp_cap) {
-          p.sp_prov[i] = -1;  // reserved but full: these rows take the atomics below
         }
       }
       uint64_t gm = 0;
@@ -1040,14 +1074,16 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
   acc.reset();
 #endif
 
+  SpillCur sc;
+  sc.init();
   // prologue: A1 of the first tile
   if (t0 < t1) {
     if (staged_tile(t0)) {
       mbar_wait(mbar, phase);
       phase ^= 1u;
-      tile_a1<NI, NF, MM, true>(p, sm, L, t0 * T, tile_rows(t0));
+      tile_a1<NI, NF, MM, true>(p, sm, L, t0 * T, tile_rows(t0), sc);
     } else {
-      tile_a1<NI, NF, MM, false>(p, sm, L, t0 * T, tile_rows(t0));
+      tile_a1<NI, NF, MM, false>(p, sm, L, t0 * T, tile_rows(t0), sc);
     }
   }
   for (int64_t tile = t0; tile < t1; ++tile) {
@@ -1094,9 +1130,9 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
       if (next_staged) {
         mbar_wait(mbar, phase);
         phase ^= 1u;
-        tile_a1<NI, NF, MM, true>(p, sm, L, base + T, tile_rows(tile + 1));
+        tile_a1<NI, NF, MM, true>(p, sm, L, base + T, tile_rows(tile + 1), sc);
       } else {
-        tile_a1<NI, NF, MM, false>(p, sm, L, base + T, tile_rows(tile + 1));
+        tile_a1<NI, NF, MM, false>(p, sm, L, base + T, tile_rows(tile + 1), sc);
       }
     }
   }
@@ -1106,6 +1142,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
 #endif
   __syncthreads();
 
+  sc.finish(p, lane);
   // ---------------- CTA table -> provisional HBM table
   const int nloc = min(misc->nlocal, Lcap);
   if (tid == 0) atomicMax(&p.dbg[1], (unsigned long long)misc->nlocal);

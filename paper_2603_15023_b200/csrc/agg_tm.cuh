@@ -239,13 +239,15 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_agg_tiles_tm(AggPlan p, SmemL
   }
   __syncthreads();
 
+  SpillCur sc;
+  sc.init();
   if (t0 < t1) {
     if (staged_tile(t0)) {
       mbar_wait(mbar, phase);
       phase ^= 1u;
-      tile_a1<NI, NF, MM, true>(p, sm, L, t0 * T, tile_rows(t0));
+      tile_a1<NI, NF, MM, true>(p, sm, L, t0 * T, tile_rows(t0), sc);
     } else {
-      tile_a1<NI, NF, MM, false>(p, sm, L, t0 * T, tile_rows(t0));
+      tile_a1<NI, NF, MM, false>(p, sm, L, t0 * T, tile_rows(t0), sc);
     }
   }
   for (int64_t tile = t0; tile < t1; ++tile) {
@@ -288,14 +290,15 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_agg_tiles_tm(AggPlan p, SmemL
       if (next_staged) {
         mbar_wait(mbar, phase);
         phase ^= 1u;
-        tile_a1<NI, NF, MM, true>(p, sm, L, base + T, tile_rows(tile + 1));
+        tile_a1<NI, NF, MM, true>(p, sm, L, base + T, tile_rows(tile + 1), sc);
       } else {
-        tile_a1<NI, NF, MM, false>(p, sm, L, base + T, tile_rows(tile + 1));
+        tile_a1<NI, NF, MM, false>(p, sm, L, base + T, tile_rows(tile + 1), sc);
       }
     }
   }
   __syncthreads();
 
+  sc.finish(p, lane);
   // ---------------- TMEM -> provisional HBM table (owners), rows and the overflow bound
   const int nloc = min(misc->nlocal, Lcap);
   if (tid == 0) atomicMax(&p.dbg[1], (unsigned long long)misc->nlocal);
