@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kThreads, PAC_MM_MINB) k_agg_minmax(AggPlan p,
 
 // ------------------------------------------------------------------ deferred HBM tier
 // Rows of groups without a CTA-local slot were appended to the spill records by tile_a1
-// (AggPlan::sp_*; the pu key is hashed here, by full warps, not in the divergent tier branch).  Instead of 64 device atomics per row on a table far larger than L2, the
+// (AggPlan::sp_*; the pu key is hashed by k_spill_resolve, by full warps, not in the divergent
+// tier branch).  Instead of 64 device atomics per row on a table far larger than L2, the
 // records are grouped by provisional slot (a counting sort: per-slot counts, slot offsets,
 // scatter of (slot, record) pairs) and each warp then folds a chunk of consecutive pairs in
 // registers, lane j holding worlds j and j+32, with one coalesced atomic flush per slot run.
@@ -234,6 +235,8 @@ __global__ void __launch_bounds__(256) k_spill_resolve(AggPlan p) {
       prov = global_slot(p, p.sp_gkey[i]);
       p.sp_prov[i] = prov;
     }
+    // the record's world mask, in place of its pu key (ALU work under the probes' latency)
+    if (prov >= 0 && !p.mask_in) p.sp_key[i] = pac_hash_dev(p.sp_key[i], p.salt);
     const unsigned peers = __match_any_sync(0xffffffffu, prov >= 0 ? (unsigned)prov : 0x80000000u | lane);
     if (prov >= 0 && lane == __ffs(peers) - 1) atomicAdd(&p.sp_cnt[prov], __popc(peers));
   }
@@ -353,8 +356,7 @@ __global__ void __launch_bounds__(256) k_spill_agg(AggPlan p, const unsigned lon
       const int2 pr = k < c1 ? pairs[k] : make_int2(-1, 0);
       unsigned long long m = 0, v[NI + NF + (MM ? 1 : 0) > 0 ? NI + NF + (MM ? 1 : 0) : 1];
       if (k < c1) {
-        const unsigned long long r = p.sp_key[pr.y];
-        m = p.mask_in ? r : pac_hash_dev(r, p.salt);
+        m = p.sp_key[pr.y];  // the mask (k_spill_resolve hashed the pu key)
 #pragma unroll
         for (int c = 0; c < NI + NF + (MM ? 1 : 0); ++c) v[c] = p.sp_val[(size_t)c * p.sp_cap + pr.y];
       }
@@ -470,38 +472,70 @@ __global__ void k_radix_hist(const unsigned long long* keys, const int* Gdev, in
 }
 
 __global__ void __launch_bounds__(1024) k_radix_scan(int* hist, int total) {
-  // exclusive scan of `total` ints by one CTA
+  // exclusive scan of `total` ints (a multiple of 256) by one CTA, 16 consecutive ints per
+  // thread per round (four 16-byte loads), so a round covers 16K counts
+  constexpr int V = 16;
   __shared__ int carry;
   __shared__ int wsum[32];
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int base = 0; base < total; base += blockDim.x) {
-    int i = base + threadIdx.x;
-    int v = i < total ? hist[i] : 0;
-    int x = v;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int base = 0; base < total; base += blockDim.x * V) {
+    const int i0 = base + threadIdx.x * V;
+    int v[V];
+    if (i0 < total) {
+#pragma unroll
+      for (int q = 0; q < V / 4; ++q) {
+        const int4 t = reinterpret_cast<const int4*>(hist + i0)[q];
+        v[4 * q] = t.x;
+        v[4 * q + 1] = t.y;
+        v[4 * q + 2] = t.z;
+        v[4 * q + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < V; ++k) v[k] = 0;
+    }
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < V; ++k) sum += v[k];
+    int x = sum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      int a = __shfl_up_sync(0xffffffffu, x, d);
+      const int a = __shfl_up_sync(0xffffffffu, x, d);
       if (lane >= d) x += a;
     }
     if (lane == 31) wsum[w] = x;
     __syncthreads();
     if (w == 0) {
-      int y = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+      const int y = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
       int yy = y;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        int a = __shfl_up_sync(0xffffffffu, yy, d);
+        const int a = __shfl_up_sync(0xffffffffu, yy, d);
         if (lane >= d) yy += a;
       }
       wsum[lane] = yy - y;
     }
     __syncthreads();
-    int excl = x - v + wsum[w] + carry;
-    if (i < total) hist[i] = excl;
+    int run = x - sum + wsum[w] + carry;
+    if (i0 < total) {
+#pragma unroll
+      for (int q = 0; q < V / 4; ++q) {
+        int4 t;
+        t.x = run;
+        run += v[4 * q];
+        t.y = run;
+        run += v[4 * q + 1];
+        t.z = run;
+        run += v[4 * q + 2];
+        t.w = run;
+        run += v[4 * q + 3];
+        reinterpret_cast<int4*>(hist + i0)[q] = t;
+      }
+    }
     __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    if (threadIdx.x == blockDim.x - 1) carry = run;
     __syncthreads();
   }
 }

@@ -720,7 +720,7 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
           if (mine) {
             p.sp_prov[i] = gprov;
             p.sp_gkey[i] = key;
-            p.sp_key[i] = tc.w8(0, li);  // hashed by k_spill_agg with full warps
+            p.sp_key[i] = tc.w8(0, li);  // hashed by k_spill_resolve with full warps
             unsigned long long* v = p.sp_val + i;
 #pragma unroll
             for (int c = 0; c < KK - 1; ++c) v[(size_t)c * p.sp_cap] = tc.w8(1 + c, li);
