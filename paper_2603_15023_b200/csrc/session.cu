@@ -59,6 +59,17 @@ __device__ __forceinline__ void cp_async16z(void* smem_dst, const void* gsrc, in
                "l"(gsrc), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc)
+               : "memory");
+}
+// 8-byte async copy of `bytes` (<= 8) source bytes, the rest zero-filled
+__device__ __forceinline__ void cp_async8z(void* smem_dst, const void* gsrc, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -77,29 +88,24 @@ struct FinPrep {
   const int64_t* num_groups;
   int64_t G_cap;
   int A;
-  int kinds[PAC_MAX_AGGS];
-  const void* world[PAC_MAX_AGGS];
-  const int64_t* count;
   const uint64_t* K;  // [G][M/64] words
   const int64_t* rows;
   uint64_t seed;
   uint32_t round;
-  double* ybuf;     // [cells][M]
   double* zbuf;     // [cells]
   uint8_t* is_null; // [cells]
   uint8_t* flags;   // [G]
 };
 
-// one warp per cell; M = 64 or 128 worlds (lane owns worlds lane + 32h, h < M/32)
+// one thread per cell: Philox block, NULL decision, normal draw, diversity flag (the y-vectors are
+// derived from the table by the chain itself, YSrc)
 template <int M>
 __global__ void k_finalize_prep(FinPrep f) {
   constexpr int W = M / 64;
   const int64_t G = min(*f.num_groups, f.G_cap);
   const int64_t cells = G * f.A;
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  for (int64_t cell = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); cell < cells;
-       cell += (int64_t)gridDim.x * wpb) {
+  for (int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < cells;
+       cell += (int64_t)gridDim.x * blockDim.x) {
     const int64_t g = cell / f.A;
     const int a = (int)(cell % f.A);
     int pc = 0;
@@ -108,28 +114,33 @@ __global__ void k_finalize_prep(FinPrep f) {
     const u32x4 x = philox4x32_10({(uint32_t)cell, (uint32_t)((uint64_t)cell >> 32), f.round, kTagCell},
                                   (uint32_t)f.seed, (uint32_t)(f.seed >> 32));
     const bool null = (int)(x.x >> (M == 64 ? 26 : 25)) >= pc;  // R10 / R29
-    const int kind = f.kinds[a];
-#pragma unroll
-    for (int h = 0; h < M / 32; ++h) {
-      const int j = lane + 32 * h;
-      const size_t c = (size_t)g * M + j;
-      double y = 0.0;
-      if ((f.K[g * W + (j >> 6)] >> (j & 63)) & 1ull) {  // R9: unset worlds read 0
-        switch (kind) {
-          case PAC_COUNT: y = 2.0 * (double)f.count[c]; break;
-          case PAC_SUM_I64: y = 2.0 * (double)((const int64_t*)f.world[a])[c]; break;
-          case PAC_SUM_F64: y = 2.0 * ((const double*)f.world[a])[c]; break;
-          case PAC_AVG_F64: y = __ddiv_rn(((const double*)f.world[a])[c], (double)f.count[c]); break;
-          default: y = ((const double*)f.world[a])[c]; break;
-        }
-      }
-      f.ybuf[cell * M + j] = y;
-    }
-    if (lane == 0) {
-      f.is_null[cell] = null ? 1 : 0;
-      f.zbuf[cell] = null ? 0.0 : normal_from(x);
-      if (a == 0 && f.flags) f.flags[g] = (f.rows[g] >= M && pc <= (M == 64 ? 34 : 68)) ? 1 : 0;  // R18 / R29
-    }
+    f.is_null[cell] = null ? 1 : 0;
+    f.zbuf[cell] = null ? 0.0 : normal_from(x);
+    if (a == 0 && f.flags) f.flags[g] = (f.rows[g] >= M && pc <= (M == 64 ? 34 : 68)) ? 1 : 0;  // R18 / R29
+  }
+}
+
+// Where the chain reads a cell's y-vector: the given vectors of pac_noised_y (ybuf[cells][M], absent
+// worlds already 0), or the aggregate table itself for pac_finalize, y derived per world in the
+// released scale (R7: 2x for COUNT/SUM, AVG = sum / count; R9: unset worlds read 0) -- no
+// [cells][M] y buffer is written and read back.
+struct YSrc {
+  const double* ybuf;
+  int kinds[PAC_MAX_AGGS];
+  const void* world[PAC_MAX_AGGS];
+  const int64_t* count;
+  const uint64_t* K;  // [G][M/64]
+};
+
+// y of one world from its staged table words: a = the world's COUNT (COUNT) or value, b = its count
+__device__ __forceinline__ double y_of(int kind, unsigned long long a, unsigned long long b, bool set) {
+  if (!set) return 0.0;
+  switch (kind) {
+    case PAC_COUNT:
+    case PAC_SUM_I64: return 2.0 * (double)(long long)a;
+    case PAC_SUM_F64: return 2.0 * __longlong_as_double((long long)a);
+    case PAC_AVG_F64: return __ddiv_rn(__longlong_as_double((long long)a), (double)(long long)b);
+    default: return __longlong_as_double((long long)a);
   }
 }
 
@@ -182,7 +193,7 @@ __device__ __forceinline__ void bayes_update(double (&p)[H], const double (&y)[H
 // one warp: the sequential release chain over M worlds (H = M/32 per lane).
 // Latency-bound (each cell's variance is taken under the posterior the previous cell left), so
 // the chain keeps two dependent warp reductions per released cell:
-//   pass 1: sum P, sum P*y, min and max of y over P > 0 (four independent trees)
+//   pass 1: sum P and sum P*y (R11's equality test beside them: ballot, broadcast, vote)
 //   pass 2: sum P*(y - mu)^2
 // and no reduction in the update: the posterior is normalised at the next released cell with the
 // mass pass 1 sums anyway (and when the chain ends), and the likelihood
@@ -193,17 +204,20 @@ __device__ __forceinline__ void bayes_update(double (&p)[H], const double (&y)[H
 // num_groups == nullptr: G_cap cells-per-aggregate rows are all valid (pac_noised_y)
 template <int M>
 __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups, int64_t G_cap, int A,
-                                                       const double* __restrict__ ybuf,
+                                                       const YSrc ys,
                                                        const double* __restrict__ zbuf,
                                                        const uint8_t* __restrict__ is_null, double* P,
                                                        unsigned long long* releases, int jstar, double B,
                                                        double* release, double* delta_out, long long* ctl) {
   constexpr int H = M / 32;
-  constexpr int CH = kChainChunk;
+  constexpr int W = M / 64;
+  constexpr int CH = kChainChunk * 64 / M;
   // cells are streamed through shared memory in chunks of CH (double-buffered cp.async), so
-  // the chain never waits on HBM latency: y-vectors, normals and NULL flags of chunk c+1 are in
-  // flight while chunk c is released
-  __shared__ __align__(16) double sy[2][CH * M];
+  // the chain never waits on HBM latency: the table rows (or y-vectors), normals and NULL flags
+  // of chunk c+1 are in flight while chunk c is released
+  __shared__ __align__(16) unsigned long long sa[2][CH * M];  // y, or the value / COUNT row
+  __shared__ __align__(16) unsigned long long sb[2][CH * M];  // the count row (AVG)
+  __shared__ __align__(16) unsigned long long sk[2][CH * 2];  // K words
   __shared__ __align__(16) double sz[2][CH];
   __shared__ __align__(16) uint8_t sn[2][CH];
   const int lane = threadIdx.x;
@@ -214,15 +228,43 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
     const int b = (int)(c & 1);
     const int64_t c0 = c * CH;
     const int nc = (int)min((int64_t)CH, cells - c0);
-    const char* gy = (const char*)(ybuf + c0 * M);
-    char* dy = (char*)sy[b];
-    for (int i = lane; i < nc * M / 2; i += 32) cp_async16(dy + 16 * i, gy + 16 * i);
+    if (ys.ybuf) {
+      const char* gy = (const char*)(ys.ybuf + c0 * M);
+      char* dy = (char*)sa[b];
+      for (int i = lane; i < nc * M / 2; i += 32) cp_async16(dy + 16 * i, gy + 16 * i);
+    } else {
+      int64_t g = c0 / A;
+      int a = (int)(c0 - g * A);
+      for (int ci = 0; ci < nc; ++ci) {
+        const int kind = ys.kinds[a];
+        const char* ra = (const char*)((kind == PAC_COUNT ? (const void*)ys.count : ys.world[a])) + g * M * 8;
+#pragma unroll
+        for (int i = lane; i < M / 2; i += 32) cp_async16((char*)(sa[b] + ci * M) + 16 * i, ra + 16 * i);
+        if (kind == PAC_AVG_F64) {
+          const char* rb = (const char*)(ys.count + g * M);
+#pragma unroll
+          for (int i = lane; i < M / 2; i += 32) cp_async16((char*)(sb[b] + ci * M) + 16 * i, rb + 16 * i);
+        }
+        if (lane == 0) {
+          if (W == 1) cp_async8(sk[b] + 2 * ci, ys.K + g);
+          else cp_async16(sk[b] + 2 * ci, ys.K + g * W);
+        }
+        if (++a == A) {
+          a = 0;
+          ++g;
+        }
+      }
+    }
     // normals: nc doubles in 16-byte pieces; NULL flags: nc bytes in one piece (zero-filled tails)
     if (lane < (nc + 1) / 2) {
       const int bytes = min(16, 8 * (nc - 2 * lane));
       cp_async16z((char*)sz[b] + 16 * lane, (const char*)(zbuf + c0) + 16 * lane, bytes);
     }
-    if (lane == 31) cp_async16z(sn[b], is_null + c0, nc);
+    if (CH == 16) {
+      if (lane == 31) cp_async16z(sn[b], is_null + c0, nc);
+    } else {  // CH = 8: chunk starts are only 8-byte aligned
+      if (lane == 31) cp_async8z(sn[b], is_null + c0, nc);
+    }
     cp_async_commit();
   };
   double p[H];
@@ -239,7 +281,8 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
   const int jl = jstar & 31, jh = jstar >> 5;
   int64_t tail = lone_world() ? 0 : cells;  // first cell left to k_finalize_tail
   if (tail > 0 && nchunks > 0) stage(0);
-  for (int64_t cell = 0; cell < tail; ++cell) {
+  int acur = 0;  // aggregate of the current cell
+  for (int64_t cell = 0; cell < tail; ++cell, acur = (acur + 1 == A) ? 0 : acur + 1) {
     const int ci = (int)(cell % CH);
     const int b = (int)((cell / CH) & 1);
     if (ci == 0) {
@@ -253,8 +296,17 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
       __syncwarp();
     }
     double y[H];
+    if (ys.ybuf) {
 #pragma unroll
-    for (int h = 0; h < H; ++h) y[h] = sy[b][ci * M + lane + 32 * h];
+      for (int h = 0; h < H; ++h) y[h] = __longlong_as_double((long long)sa[b][ci * M + lane + 32 * h]);
+    } else {
+      const int kind = ys.kinds[acur];
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const int j = lane + 32 * h;
+        y[h] = y_of(kind, sa[b][ci * M + j], sb[b][ci * M + j], (sk[b][2 * ci + (j >> 6)] >> (j & 63)) & 1ull);
+      }
+    }
     if (sn[b][ci]) {
       if (lane == 0) {
         release[cell] = NAN;
@@ -352,7 +404,7 @@ __global__ void __launch_bounds__(32) k_finalize_chain(const int64_t* num_groups
 // is NaN, every other cell is a zero-variance release of y_{j*} (R11: with one world there is
 // nothing to compare), and P no longer changes -- so the rest of the chain is cell-parallel.
 template <int M>
-__global__ void k_finalize_tail(const int64_t* num_groups, int64_t G_cap, int A, const double* __restrict__ ybuf,
+__global__ void k_finalize_tail(const int64_t* num_groups, int64_t G_cap, int A, const YSrc ys,
                                 const uint8_t* __restrict__ is_null, int jstar, double* release, double* delta_out,
                                 const long long* ctl) {
   const int64_t G = num_groups ? min(*num_groups, G_cap) : G_cap;
@@ -361,7 +413,22 @@ __global__ void k_finalize_tail(const int64_t* num_groups, int64_t G_cap, int A,
   for (int64_t cell = ctl[kCtlTail] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < cells;
        cell += stride) {
     const bool null = is_null[cell] != 0;
-    release[cell] = null ? NAN : ybuf[cell * M + jstar];
+    double yj = 0.0;
+    if (!null) {
+      if (ys.ybuf) {
+        yj = ys.ybuf[cell * M + jstar];
+      } else {
+        const int64_t g = cell / A;
+        const int a = (int)(cell - g * A);
+        const int kind = ys.kinds[a];
+        const size_t c = (size_t)g * M + jstar;
+        const unsigned long long va = kind == PAC_COUNT ? (unsigned long long)ys.count[c]
+                                                        : ((const unsigned long long*)ys.world[a])[c];
+        const unsigned long long vb = kind == PAC_AVG_F64 ? (unsigned long long)ys.count[c] : 0ull;
+        yj = y_of(kind, va, vb, (ys.K[g * (M / 64) + (jstar >> 6)] >> (jstar & 63)) & 1ull);
+      }
+    }
+    release[cell] = null ? NAN : yj;
     if (delta_out) delta_out[cell] = null ? NAN : 0.0;
   }
 }
@@ -375,10 +442,10 @@ __global__ void __launch_bounds__(32) k_posterior_update(double* P, const double
   P[lane + 32] = p[1];
 }
 
-// workspace: y-vectors [cells][M], normals [cells], chain control block (64 B)
-static size_t fin_ws(int64_t G_cap, int A, size_t* o_z, size_t* o_c, int M = kM) {
+// workspace: [y-vectors [cells][M], pac_noised_y only], normals [cells], chain control block (64 B)
+static size_t fin_ws(int64_t G_cap, int A, bool with_y, size_t* o_z, size_t* o_c, int M = kM) {
   const size_t cells = (size_t)G_cap * A;
-  size_t y = cells * M * 8;
+  const size_t y = with_y ? cells * M * 8 : 0;
   *o_z = (y + 255) & ~(size_t)255;
   size_t z = cells * 8;
   *o_c = (*o_z + z + 255) & ~(size_t)255;
@@ -388,15 +455,15 @@ static size_t fin_ws(int64_t G_cap, int A, size_t* o_z, size_t* o_c, int M = kM)
 // the release chain: the sequential part, then the cell-parallel tail (empty unless the
 // posterior's support shrank to one world)
 template <int M>
-static void launch_chain(const int64_t* num_groups, int64_t G_cap, int A, const double* ybuf, const double* zbuf,
+static void launch_chain(const int64_t* num_groups, int64_t G_cap, int A, const YSrc& ys, const double* zbuf,
                          const uint8_t* is_null, pac_session* s, double* release, double* delta_out, long long* ctl,
                          cudaStream_t st) {
-  k_finalize_chain<M><<<1, 32, 0, st>>>(num_groups, G_cap, A, ybuf, zbuf, is_null, s->d_P, s->d_count, s->jstar,
+  k_finalize_chain<M><<<1, 32, 0, st>>>(num_groups, G_cap, A, ys, zbuf, is_null, s->d_P, s->d_count, s->jstar,
                                         s->B, release, delta_out, ctl);
   note_launch();
   const int64_t cells = G_cap * A;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((cells + 255) / 256, 148 * 8));
-  k_finalize_tail<M><<<blocks, 256, 0, st>>>(num_groups, G_cap, A, ybuf, is_null, s->jstar, release, delta_out, ctl);
+  k_finalize_tail<M><<<blocks, 256, 0, st>>>(num_groups, G_cap, A, ys, is_null, s->jstar, release, delta_out, ctl);
   note_launch();
 }
 
@@ -472,8 +539,8 @@ extern "C" double* pac_session_posterior_device(pac_session* s) { return s ? s->
 
 extern "C" int pac_finalize_workspace_size(int64_t G_cap, int n_aggs, size_t* bytes) {
   if (!bytes || G_cap < 1 || n_aggs < 1 || n_aggs > PAC_MAX_AGGS) return PAC_E_INVAL;
-  size_t oz, on;
-  *bytes = fin_ws(G_cap, n_aggs, &oz, &on, 128);  // enough for m = 64 and m = 128 tables
+  size_t oz, oc;
+  *bytes = fin_ws(G_cap, n_aggs, false, &oz, &oc, 128);
   return PAC_OK;
 }
 
@@ -495,7 +562,7 @@ extern "C" int pac_finalize(pac_session* s, const pac_table* t, const pac_agg_sp
   const int M = t->m ? t->m : 64;
   if (M != s->m) return PAC_E_INVAL;  // the table and the session must agree on m (R29)
   size_t oz, oc;
-  const size_t need = fin_ws(G_cap, n_aggs, &oz, &oc, M);
+  const size_t need = fin_ws(G_cap, n_aggs, false, &oz, &oc, M);
   if (!d_ws || ws_bytes < need) return PAC_E_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)d_ws;
@@ -503,30 +570,31 @@ extern "C" int pac_finalize(pac_session* s, const pac_table* t, const pac_agg_sp
   f.num_groups = t->d_num_groups;
   f.G_cap = G_cap;
   f.A = n_aggs;
-  for (int a = 0; a < n_aggs; ++a) {
-    f.kinds[a] = aggs[a].kind;
-    f.world[a] = t->d_world[a];
-  }
-  f.count = t->d_count;
   f.K = t->d_presence;
   f.rows = t->d_rows;
   f.seed = s->seed;
   f.round = round;
-  f.ybuf = (double*)ws;
   f.zbuf = (double*)(ws + oz);
   f.is_null = d_is_null;
   f.flags = d_flags;
+  YSrc ys{};
+  for (int a = 0; a < n_aggs; ++a) {
+    ys.kinds[a] = aggs[a].kind;
+    ys.world[a] = t->d_world[a];
+  }
+  ys.count = t->d_count;
+  ys.K = t->d_presence;
   const int64_t cells = G_cap * n_aggs;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((cells + 7) / 8, 148 * 32));
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((cells + 255) / 256, 148 * 8));
   long long* ctl = (long long*)(ws + oc);
   if (M == 64) {
     k_finalize_prep<64><<<blocks, 256, 0, st>>>(f);
     note_launch();
-    launch_chain<64>(t->d_num_groups, G_cap, n_aggs, f.ybuf, f.zbuf, d_is_null, s, d_release, d_delta, ctl, st);
+    launch_chain<64>(t->d_num_groups, G_cap, n_aggs, ys, f.zbuf, d_is_null, s, d_release, d_delta, ctl, st);
   } else {
     k_finalize_prep<128><<<blocks, 256, 0, st>>>(f);
     note_launch();
-    launch_chain<128>(t->d_num_groups, G_cap, n_aggs, f.ybuf, f.zbuf, d_is_null, s, d_release, d_delta, ctl, st);
+    launch_chain<128>(t->d_num_groups, G_cap, n_aggs, ys, f.zbuf, d_is_null, s, d_release, d_delta, ctl, st);
   }
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
@@ -542,8 +610,8 @@ extern "C" int pac_posterior_update(pac_session* s, const double* d_y64, double 
 
 extern "C" int pac_noised_y_workspace_size(int64_t n, size_t* bytes) {
   if (!bytes || n < 0) return PAC_E_INVAL;
-  size_t oz, on;
-  *bytes = fin_ws(n > 0 ? n : 1, 1, &oz, &on);
+  size_t oz, oc;
+  *bytes = fin_ws(n > 0 ? n : 1, 1, true, &oz, &oc);
   return PAC_OK;
 }
 
@@ -554,7 +622,7 @@ extern "C" int pac_noised_y(pac_session* s, const double* d_y, const uint64_t* d
     return PAC_E_INVAL;
   if (n == 0) return PAC_OK;
   size_t oz, oc;
-  const size_t need = fin_ws(n, 1, &oz, &oc);
+  const size_t need = fin_ws(n, 1, true, &oz, &oc);
   if (!d_ws || ws_bytes < need) return PAC_E_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)d_ws;
@@ -563,6 +631,8 @@ extern "C" int pac_noised_y(pac_session* s, const double* d_y, const uint64_t* d
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, 148 * 32));
   k_noised_prep_y<<<blocks, 256, 0, st>>>(d_y, d_presence, n, s->seed, round, ybuf, zbuf, d_is_null);
   note_launch();
-  launch_chain<64>(nullptr, n, 1, ybuf, zbuf, d_is_null, s, d_release, d_delta, (long long*)(ws + oc), st);
+  YSrc ys{};
+  ys.ybuf = ybuf;
+  launch_chain<64>(nullptr, n, 1, ys, zbuf, d_is_null, s, d_release, d_delta, (long long*)(ws + oc), st);
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
