@@ -261,6 +261,7 @@ __device__ __forceinline__ uint64_t row_group_key(const AggPlan& p, int64_t r) {
   return packed;
 }
 
+// ------------------------------------------------------------------ TMA bulk staging
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }

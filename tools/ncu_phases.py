@@ -8,7 +8,7 @@ def find(pat):
     for i, l in enumerate(src, 1):
         if re.search(pat, l):
             return i
-    raise SystemExit("pattern not found: " + pat)
+    return 10**9  # region marker absent in this source version
 marks = [("dict/local_code", find(r"^static __device__ int local_code")),
          ("row_group_key", find(r"uint64_t row_group_key")),
          ("tma helpers", find(r"^// ------------------------------------------------------------------ TMA bulk")),
