@@ -457,8 +457,34 @@ __global__ void __launch_bounds__(1024) k_sort_small(const unsigned long long* k
 // order -> stable scatter (warp-synchronous, chunk processed in order by one warp).
 constexpr int kRadixChunk = 2048;
 
+// OR and AND of all keys (rng[0], rng[1], preset to 0 and ~0): a pass whose digit is the same in
+// every key is an identity permutation, so its histogram and scan are skipped and its scatter
+// is a copy (a packed int32 group key leaves four of the eight passes constant).
+__global__ void k_radix_range(const unsigned long long* keys, const int* Gdev, unsigned long long* rng) {
+  const int G = *Gdev;
+  unsigned long long o = 0, a = ~0ull;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < G; i += gridDim.x * blockDim.x) {
+    o |= keys[i];
+    a &= keys[i];
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    o |= __shfl_xor_sync(0xffffffffu, o, d);
+    a &= __shfl_xor_sync(0xffffffffu, a, d);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(&rng[0], o);
+    atomicAnd(&rng[1], a);
+  }
+}
+
+__device__ __forceinline__ bool radix_digit_constant(const unsigned long long* rng, int shift) {
+  return rng && (((rng[0] ^ rng[1]) >> shift) & 255ull) == 0;
+}
+
 __global__ void k_radix_hist(const unsigned long long* keys, const int* Gdev, int shift,
-                             int* hist /*[256][nblocks]*/, int nblocks) {
+                             int* hist /*[256][nblocks]*/, int nblocks, const unsigned long long* rng) {
+  if (radix_digit_constant(rng, shift)) return;
   __shared__ int h[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
   __syncthreads();
@@ -471,7 +497,9 @@ __global__ void k_radix_hist(const unsigned long long* keys, const int* Gdev, in
   for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[d * nblocks + b] = h[d];
 }
 
-__global__ void __launch_bounds__(1024) k_radix_scan(int* hist, int total) {
+__global__ void __launch_bounds__(1024) k_radix_scan(int* hist, int total, const unsigned long long* rng,
+                                                     int shift) {
+  if (radix_digit_constant(rng, shift)) return;
   // exclusive scan of `total` ints (a multiple of 256) by one CTA, 16 consecutive ints per
   // thread per round (four 16-byte loads), so a round covers 16K counts
   constexpr int V = 16;
@@ -541,7 +569,17 @@ __global__ void __launch_bounds__(1024) k_radix_scan(int* hist, int total) {
 }
 
 __global__ void k_radix_scatter(const unsigned long long* kin, const int* iin, unsigned long long* kout,
-                                int* iout, const int* Gdev, int shift, const int* hist, int nblocks) {
+                                int* iout, const int* Gdev, int shift, const int* hist, int nblocks,
+                                const unsigned long long* rng) {
+  if (radix_digit_constant(rng, shift)) {  // identity permutation: copy through
+    const int G = *Gdev;
+    const int lo = blockIdx.x * kRadixChunk, hi = min(G, lo + kRadixChunk);
+    for (int i = lo + (int)threadIdx.x; i < hi; i += blockDim.x) {
+      kout[i] = kin[i];
+      iout[i] = iin ? iin[i] : i;
+    }
+    return;
+  }
   // one warp per block, processes its chunk in order -> stable
   __shared__ int base[256];
   const int b = blockIdx.x, lane = threadIdx.x;
@@ -708,7 +746,7 @@ static WsLayout ws_layout(const AccSet& A, int64_t G_cap) {
   w.Hcap = next_pow2(std::max<int64_t>(2 * Gc, 64));
   w.o_gkey = take(8 * w.Hcap);
   w.o_gstate = take(4 * w.Hcap);
-  w.o_ctr = take(64);  // gcounter, Gdev, gmaxabs, dbg[2], spill records reserved, spill records grouped
+  w.o_ctr = take(64);  // gcounter, Gdev, gmaxabs, dbg[2], spill records reserved / grouped, key OR / AND
   w.o_pkey = take(8 * Gc);
   w.o_prows = take(8 * Gc);
   w.o_pcount = A.has_count ? take(8 * Gc * kM) : 0;
@@ -1216,13 +1254,18 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
     int* hist = (int*)(ws + W.o_hist);
     const unsigned long long* kin = p.prov_key;
     const int* iin = nullptr;
+    unsigned long long* rng = (unsigned long long*)(ws + W.o_ctr + 48);  // OR, AND of the keys
+    if (cudaMemsetAsync(rng + 1, 0xFF, 8, st) != cudaSuccess) return PAC_E_CUDA;
+    k_radix_range<<<(int)std::min<int64_t>((G_cap + 255) / 256, (int64_t)sms * 4), 256, 0, st>>>(p.prov_key, Gdev,
+                                                                                                 rng);
+    note_launch();
     for (int pass = 0; pass < 8; ++pass) {
       unsigned long long* ko = (pass & 1) ? k1 : k0;
       int* io = (pass & 1) ? i1 : i0;
       if (pass == 7) io = perm;
-      k_radix_hist<<<W.nblocks, 256, 0, st>>>(kin, Gdev, 8 * pass, hist, W.nblocks);
-      k_radix_scan<<<1, 1024, 0, st>>>(hist, 256 * W.nblocks);
-      k_radix_scatter<<<W.nblocks, 32, 0, st>>>(kin, iin, ko, io, Gdev, 8 * pass, hist, W.nblocks);
+      k_radix_hist<<<W.nblocks, 256, 0, st>>>(kin, Gdev, 8 * pass, hist, W.nblocks, rng);
+      k_radix_scan<<<1, 1024, 0, st>>>(hist, 256 * W.nblocks, rng, 8 * pass);
+      k_radix_scatter<<<W.nblocks, 32, 0, st>>>(kin, iin, ko, io, Gdev, 8 * pass, hist, W.nblocks, rng);
       for (int q = 0; q < 3; ++q) note_launch();
       kin = ko;
       iin = io;
