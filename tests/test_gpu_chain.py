@@ -99,3 +99,30 @@ def test_nan_before_collapse_poisons_posterior_like_the_oracle(orc):
     f = ~np.isnan(r_o)
     np.testing.assert_allclose(rel[f], r_o[f], rtol=1e-9, atol=0)
     np.testing.assert_array_equal(np.isnan(s.query()["P"]), np.isnan(P))
+
+
+def test_table_chain_collapse_and_tail_match_oracle(orc):
+    """pac_finalize on a C3-shaped table (many small groups): the chain derives y from the table
+    rows, the posterior collapses within the first call and k_finalize_tail releases the rest;
+    the second call starts collapsed (tail only).  Parity with the oracle both times."""
+    import datagen as dg
+    from gpu_helpers import run_gpu, workload_aggs
+    w = dg.WORKLOADS["C3"]
+    cols = w.host_columns(0, 400_000)
+    aggs = workload_aggs(w, cols)
+    seed = 2024
+    jstar, salt, P = orc.session(seed)
+    s = pac.Session(seed, w.budget)
+    t, _ = run_gpu(aggs, cols["keys"], pu=cols["pu"], salt=salt, G_cap=1 << 17)
+    ref = orc.agg(orc.pac_hash(cols["pu"], salt), cols["keys"], aggs)
+    G = ref["G"]
+    fin = pac.Finalizer(t.kinds, t.G_cap)
+    for rnd in range(2):
+        rel, isn, flags, delta = fin(s, t, rnd)
+        r_o, n_o, f_o, d_o, P = orc.finalize(seed, w.budget, jstar, P, ref, rnd)
+        rel = rel[:G].cpu().numpy()
+        isn = isn[:G].cpu().numpy()
+        assert_releases_close(rel, r_o, d_o, isn, n_o)
+        np.testing.assert_array_equal(flags[:G].cpu().numpy(), f_o)
+        np.testing.assert_allclose(s.query()["P"], P, rtol=0, atol=1e-9)
+    assert (P > 0).sum() == 1  # collapsed: the tail kernel carried most of both calls
