@@ -1200,7 +1200,9 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
         for (int i = 0; i < p.nraw; ++i) copied += L.T * p.raw_eb[i];
         p.raw_bytes = copied;
         p.tma_ok = (aligned && !getenv("PAC_NO_TMA")) ? 1 : 0;
+#ifdef PAC_ABLATE_BUILD
         p.ablate = getenv("PAC_ABLATE") ? atoi(getenv("PAC_ABLATE")) : 0;
+#endif
       }
       if (getenv("PAC_DEBUG"))
         fprintf(stderr, "[libpac] k_agg_tiles%s<%d,%d,%d> T=%d Lcap=%d LH=%d smem=%d B (G_cap=%lld)\n",
