@@ -759,6 +759,8 @@ __device__ __forceinline__ void tile_a1(const AggPlan& p, const TileSmem& sm, co
     unsigned short* uc = sm.ucnt + (li >> 5) * Lcap;
     if (Lcap <= 32) {  // this unit's counts start at zero
       if (lane < Lcap) uc[lane] = 0;
+    } else if ((Lcap & 3) == 0) {  // 8-byte stores (a unit's row is Lcap * 2 bytes, 8-aligned)
+      for (int z = lane; z < (Lcap >> 2); z += 32) reinterpret_cast<uint2*>(uc)[z] = make_uint2(0u, 0u);
     } else {
       for (int z = lane; z < Lcap; z += 32) uc[z] = 0;
     }
