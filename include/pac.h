@@ -46,7 +46,9 @@ enum {
   PAC_E_CAPACITY = 2,   /* more distinct groups than G_cap (pac_table_check) */
   PAC_E_WORKSPACE = 3,  /* ws_bytes smaller than the *_workspace_size() answer */
   PAC_E_CUDA = 4,       /* a CUDA runtime call or kernel launch failed */
-  PAC_E_OVERFLOW = 5    /* an int64 world sum overflowed (R15 precondition violated) */
+  PAC_E_OVERFLOW = 5,   /* an int64 world sum overflowed (R15 precondition violated) */
+  PAC_E_MERGE = 6       /* pac_merge_unpack: the ranks' tables were not laid out on one
+                           group dictionary (fingerprints differ) */
 };
 
 /* Aggregate kinds (agg in {sum, count, avg, min, max}).  Values: SUM_I64 reads
@@ -124,6 +126,11 @@ int pac_mask(const int64_t* d_pu_key, int64_t n, uint64_t salt, uint64_t* d_mask
  *                                  SUM_F64 / AVG_F64 (the world's value SUM -- AVG
  *                                  divides by d_count at finalize, R6) and MIN/MAX
  *                                  (+inf / -inf for a world with no row); NULL for COUNT
+ * Non-finite values (R30, R31): f64 SUM/AVG are IEEE sums (any NaN -> NaN, +inf with -inf
+ * -> NaN, else the infinity; finite sums that overflow are out of contract); MIN/MAX use
+ * DuckDB's total order on DOUBLE -- NaN above +inf, all NaNs equal (a NaN is written as the
+ * canonical quiet NaN).  A world holding only +inf under MIN reads +inf like an empty
+ * world; d_presence tells them apart.
  */
 typedef struct {
   int64_t* d_num_groups;
@@ -177,8 +184,11 @@ int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, uint64_t sa
 int pac_table_check(const pac_table* t, int64_t* h_num_groups, pac_stream_t stream);
 
 /* Re-derives K after a cross-GPU merge (NCCL has no bitwise-OR reduction, §8e):
- * K[g] bit j = (count[g][j] > 0) when d_count is present, else (the MIN or MAX world
- * value is not its empty sentinel).  Uses the device-side num_groups. */
+ * K[g] bit j = (count[g][j] > 0) when d_count is present (R5, exact).  MIN/MAX-only tables
+ * have no counts and a world holding only +inf (MIN) / -inf (MAX) looks empty in the f64
+ * table, so there the caller must merge d_presence itself (OR across ranks) and this call
+ * only ORs in the worlds whose MIN is not +inf or MAX is not -inf (it never clears a bit).
+ * Uses the device-side num_groups. */
 int pac_table_rederive_presence(const pac_table* t, const pac_agg_spec* aggs, int n_aggs,
                                 int64_t G_cap, pac_stream_t stream);
 
@@ -186,10 +196,39 @@ int pac_table_rederive_presence(const pac_table* t, const pac_agg_spec* aggs, in
  * laid out by the ascending union dictionary d_union_keys[G_union]; groups absent from
  * `in` get the empty state (count 0, sums 0, MIN +inf, MAX -inf, rows 0, K 0).  Used so
  * that all ranks share one layout before the allreduce.  `in`'s num_groups is read
- * from the device. */
+ * from the device and clamped to G_cap_in; `out`'s status is `in`'s. */
 int pac_table_remap(const pac_table* in, const uint64_t* d_union_keys, int64_t G_union,
                     const pac_agg_spec* aggs, int n_aggs, int64_t G_cap_in,
                     const pac_table* out, pac_stream_t stream);
+
+/* ------------------------------------------------------------------ cross-GPU merge (§8 a5/e)
+ * The combine of row-sharded partial tables (P:L1777, P:L1966, P:L2010 thread-local states +
+ * combine) as three NCCL all_reduce calls over flat buffers, with no host synchronisation.
+ * Every rank's table must be laid out on one group dictionary (pac_table_remap onto the sorted
+ * union, or identical dense domains); a fingerprint of the dictionary travels with the data
+ * and a mismatch is detected on the device.  Buffers (caller-allocated device memory, element
+ * counts from pac_merge_sizes; G = G_cap, fixed, so no num_groups read on the host):
+ *   d_i64_sum [n_i64_sum] int64  all_reduce SUM: rows [G], count [G][64] (if the table has
+ *                                counts), per SUM_I64 aggregate [G][64]
+ *   d_f64_sum [n_f64_sum] double all_reduce SUM: per SUM_F64 / AVG_F64 aggregate [G][64]
+ *                                (may be NULL when n_f64_sum == 0)
+ *   d_i64_min [n_i64_min] int64  all_reduce MIN: dictionary fingerprint f and ~f, ~status,
+ *                                per MIN aggregate [G][64] order-preserving encodings of the
+ *                                extremes (R31, NaN largest), per MAX aggregate [G][64] their
+ *                                bitwise NOT; a world not in K packs the empty sentinel.
+ * pac_merge_unpack writes the merged rows, counts, worlds and K back into the table: K =
+ * {count > 0} (R5) or, for MIN/MAX-only tables, the worlds whose merged extreme is not the
+ * sentinel (the OR of the ranks' K, exact even for worlds holding only +inf / -inf); d_status
+ * = the largest status of any rank, or PAC_E_MERGE when the fingerprints differ.  The int64
+ * sums wrap like any int64 addition (R15 precondition: |world sum| < 2^63 globally).
+ * Errors: PAC_E_INVAL (bad sizes / pointers, m != 64), PAC_E_CUDA. */
+int pac_merge_sizes(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, int64_t* n_i64_sum,
+                    int64_t* n_f64_sum, int64_t* n_i64_min);
+int pac_merge_pack(const pac_table* t, const pac_agg_spec* aggs, int n_aggs, int64_t G_cap,
+                   int64_t* d_i64_sum, double* d_f64_sum, int64_t* d_i64_min, pac_stream_t stream);
+int pac_merge_unpack(const pac_table* t, const pac_agg_spec* aggs, int n_aggs, int64_t G_cap,
+                     const int64_t* d_i64_sum, const double* d_f64_sum, const int64_t* d_i64_min,
+                     pac_stream_t stream);
 
 /* ------------------------------------------------------------------ m = 128 worlds (§8 f4)
  * P:L92 (§2): "Extending to m=128 is possible, and worst-case would double the cost".
@@ -221,8 +260,13 @@ int pac_agg_grouped128(const int64_t* d_pu_key, const uint64_t* d_mask2, uint64_
  *        P <- P*W/sum(P*W), W_j = exp(-(d_j - min d)/(2 Delta))         (R14)
  * Outputs (caller-allocated, [G_cap][n_aggs] unless noted):
  *   d_release (NaN for NULL cells), d_is_null (0/1), d_flags [G_cap] bit 0 = diversity
- *   check (rows >= 64 and popcount K <= 34, R18), d_delta (optional, may
- *   be NULL; NaN for NULL cells).
+ *   check (rows >= 64 and popcount K <= 34, R18), bit 1 = the table's
+ *   d_status was nonzero (CAPACITY / OVERFLOW: then every cell is NULL and P is left
+ *   unchanged -- nothing is released from an invalid table), d_delta (optional, may be
+ *   NULL; NaN for NULL cells).
+ * SURVEY §8(b) lists PAC_E_SUSPICIOUS as a return code for a diversity-flagged group; the
+ * call is asynchronous (the flags exist only on the device when it returns), so the
+ * diversity check is reported in d_flags bit 0 instead and never aborts (R18).
  * The session posterior is updated in place on the device, in cell order.
  * Errors: PAC_E_INVAL, PAC_E_WORKSPACE, PAC_E_CUDA. */
 int pac_finalize_workspace_size(int64_t G_cap, int n_aggs, size_t* bytes);
@@ -313,18 +357,24 @@ int pac_join_table_status(const void* d_table, pac_stream_t stream);
  * d_tables is a HOST array of k device table pointers).  Join elimination (Eq. join-elim):
  * the final x is the PU key; d_mask[i] = pac_hash(x, salt) (R1, R2), or 0 when some lookup
  * finds no match (R27: no PU -> in no world; pac_agg_grouped drops the row, R21).  Either
- * output may be NULL (d_pu_key[i] = x, or 0 without a match). */
+ * output may be NULL (d_pu_key[i] = x, or 0 without a match).  0 is also a valid PU key, so
+ * d_pu_key cannot mark an unmatched row: aggregate joined rows through d_mask (passed as
+ * pac_agg_grouped's d_mask, which drops the unmatched rows), never by feeding d_pu_key back
+ * as pac_agg_grouped's d_pu_key when some row may be unmatched. */
 int pac_join_mask(const void* const* d_tables, int k, const int64_t* d_fk, int64_t n, uint64_t salt,
                   uint64_t* d_mask, int64_t* d_pu_key, pac_stream_t stream);
 
 /* ------------------------------------------------------------------ runtime / profiling
  * Number of kernels this library has launched since load (all entry points). */
 uint64_t pac_launch_count(void);
-/* When enabled, pac_agg_grouped brackets its main aggregation kernel with CUDA events
- * on `stream` and accumulates the elapsed time; pac_profile_read synchronizes on the
+/* When enabled, pac_agg_grouped brackets its aggregation pass (the main kernel, plus the
+ * deferred HBM tier's kernels when they run) with CUDA events on `stream` and accumulates the elapsed time; pac_profile_read synchronizes on the
  * recorded events and returns (total ms, number of timed launches), then resets. */
 int pac_profile_enable(int on);
 int pac_profile_read(double* h_total_ms, int64_t* h_launches);
+/* Name of the kernel(s) of the last timed region (e.g. "k_agg_tiles_tm<1,1,0>"; the deferred
+ * HBM tier's kernels are inside the region when they ran).  Owned by the library. */
+const char* pac_profile_last_kernel(void);
 /* Library version string. */
 const char* pac_version(void);
 

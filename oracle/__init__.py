@@ -201,6 +201,73 @@ def agg(masks: np.ndarray, key_cols: Sequence[np.ndarray], aggs: Sequence[tuple]
             "kinds": [k for k, _ in aggs], "overflow": bool(ovf)}
 
 
+def _table_ptrs(t):
+    return (t["rows"], t["K"], t["count"],
+            (ctypes.c_void_p * max(1, len(t["world"])))(*[None if w is None else w.ctypes.data for w in t["world"]]))
+
+
+def combine(a: dict, b: dict) -> dict:
+    """a <- a (+) b (state.combine, P:L1966 / P:L2010) for two partial tables over the same
+    groups; returns a."""
+    assert a["G"] == b["G"] and np.array_equal(a["keys"], b["keys"])
+    kinds = np.array(a["kinds"], dtype=np.int32)
+    ra, Ka, ca, wa = _table_ptrs(a)
+    rb, Kb, cb, wb = _table_ptrs(b)
+    L = _load()
+    L.orc_combine.restype = ctypes.c_int
+    L.orc_combine.argtypes = [ctypes.c_int64, _P, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _P]
+    ovf = L.orc_combine(a["G"], _ptr(kinds), len(kinds), _ptr(ra), _ptr(Ka), _ptr(ca), wa,
+                        _ptr(rb), _ptr(Kb), _ptr(cb), wb)
+    a["overflow"] = bool(a["overflow"] or b["overflow"] or ovf)
+    return a
+
+
+def _ranges(n: int, parts: int):
+    parts = max(1, min(parts, max(1, n)))
+    return [(n * i // parts, n * (i + 1) // parts) for i in range(parts)]
+
+
+def pac_hash_mt(keys: np.ndarray, salt: int, threads: int) -> np.ndarray:
+    """pac_hash on `threads` host threads (contiguous row ranges; ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    keys = np.ascontiguousarray(keys, dtype=np.int64)
+    out = np.empty(keys.shape[0], dtype=np.uint64)
+    L = _load()
+
+    def run(r):
+        a, b = r
+        if b > a:
+            L.orc_pac_hash_n(keys[a:].ctypes.data, b - a, salt & 0xFFFFFFFFFFFFFFFF, out[a:].ctypes.data)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, _ranges(len(keys), threads)))
+    return out
+
+
+def agg_mt(masks: np.ndarray, key_cols: Sequence[np.ndarray], aggs: Sequence[tuple], threads: int) -> dict:
+    """O2 on `threads` host threads: each thread runs O2 on a contiguous row range (group keys per
+    range, then their sorted union), the partial tables are combined in thread order (SURVEY
+    §8c O2 "per-thread states, merged in thread order").  CPU-baseline timing only."""
+    from concurrent.futures import ThreadPoolExecutor
+    masks = np.ascontiguousarray(masks, dtype=np.uint64)
+    key_cols = [np.ascontiguousarray(c) for c in key_cols]
+    aggs = [(k, None if v is None else np.ascontiguousarray(v)) for k, v in aggs]
+    rng = _ranges(masks.shape[0], threads)
+    with ThreadPoolExecutor(threads) as ex:
+        parts = list(ex.map(lambda r: group_keys([c[r[0]:r[1]] for c in key_cols], masks[r[0]:r[1]]), rng))
+    gk = np.unique(np.concatenate(parts)) if parts else np.zeros(0, dtype=np.uint64)
+    if not key_cols:
+        gk = np.zeros(1, dtype=np.uint64)
+    sub = lambda r: agg(masks[r[0]:r[1]], [c[r[0]:r[1]] for c in key_cols],
+                        [(k, None if v is None else v[r[0]:r[1]]) for k, v in aggs], gkeys=gk)
+    with ThreadPoolExecutor(threads) as ex:
+        tabs = list(ex.map(sub, rng))
+    out = tabs[0]
+    for t in tabs[1:]:
+        combine(out, t)
+    return out
+
+
 def agg_from_keys(pu_keys: np.ndarray, salt: int, key_cols, aggs, gkeys=None, method="o2") -> dict:
     return agg(pac_hash(pu_keys, salt), key_cols, aggs, gkeys=gkeys, method=method)
 

@@ -210,12 +210,29 @@ static int64_t find_group(const uint64_t* gkeys, int64_t G, uint64_t key) {
 enum { K_COUNT = 0, K_SUM_I64 = 1, K_SUM_F64 = 2, K_AVG_F64 = 3, K_MIN_F64 = 4, K_MAX_F64 = 5 };
 
 /* Neumaier-compensated running sum (oracle-side accuracy only; the definition is
- * the exact sum). */
+ * the exact sum).  DESIGN.md R30 (non-finite terms): the IEEE-754 sum -- any NaN
+ * term gives NaN, +inf and -inf together give NaN, otherwise an infinite term gives
+ * that infinity.  Once a term or the running sum is non-finite the compensation is
+ * dropped and the plain IEEE addition continues (the compensation of finite terms
+ * would otherwise turn inf into inf - inf = NaN). */
 typedef struct { double s, c; } csum;
 static void csum_add(csum* a, double v) {
+  if (!isfinite(v) || !isfinite(a->s)) { a->s += v; return; }
   double t = a->s + v;
+  if (!isfinite(t)) { a->s = t; return; }  /* finite overflow: out of contract (R30) */
   if (fabs(a->s) >= fabs(v)) a->c += (a->s - t) + v; else a->c += (v - t) + a->s;
   a->s = t;
+}
+static double csum_value(const csum* a) { return isfinite(a->s) ? a->s + a->c : a->s; }
+
+/* DESIGN.md R31: MIN/MAX order doubles by DuckDB's total order (the paper's host system,
+ * P:L1966; r_j = agg({...}) P:L957-970 with agg = the DBMS's min/max): NaN is larger than
+ * every other value (+inf included) and all NaNs are equal; otherwise IEEE order.
+ * tot_less(a, b) is a < b in that order. */
+static int tot_less(double a, double b) {
+  if (isnan(a)) return 0;
+  if (isnan(b)) return 1;
+  return a < b;
 }
 
 /* Output table, canonical group order (ascending packed key = gkeys):
@@ -271,13 +288,13 @@ int orc_agg_o2(const uint64_t* masks, int64_t n, const void* const* cols, const 
           case K_MIN_F64: {
             double v = ((const double*)values[a])[r];
             double* e = &((double*)world[a])[cell];
-            if (v < *e) *e = v;
+            if (count[cell] == 1 || tot_less(v, *e)) *e = v;
             break;
           }
           case K_MAX_F64: {
             double v = ((const double*)values[a])[r];
             double* e = &((double*)world[a])[cell];
-            if (v > *e) *e = v;
+            if (count[cell] == 1 || tot_less(*e, v)) *e = v;
             break;
           }
           default: break;
@@ -293,12 +310,56 @@ int orc_agg_o2(const uint64_t* masks, int64_t n, const void* const* cols, const 
         if (s > (__int128)INT64_MAX || s < (__int128)INT64_MIN) overflow = 1;
         ((int64_t*)world[a])[cell] = (int64_t)s;
       } else if (kinds[a] == K_SUM_F64 || kinds[a] == K_AVG_F64) {
-        ((double*)world[a])[cell] = fsum[idx].s + fsum[idx].c;
+        ((double*)world[a])[cell] = csum_value(&fsum[idx]);
       }
     }
   }
   free(isum);
   free(fsum);
+  return overflow;
+}
+
+/* combine: state.combine(other) of two partial tables over the same groups ("thread-
+ * local" states, P:L2010 combine; O2 "merge per-thread states in thread order"):
+ * a <- a (+) b.  rows, counts and int64 sums add (returns 1 when an int64 world sum leaves the
+ * int64 range, checked with __int128 -- exact when neither partial overflowed), K ORs, f64 sums
+ * add (IEEE, R30), MIN/MAX keep the total-order extreme (R31) of the worlds non-empty in a or b
+ * (emptiness from the counts).  Used only to time O2 on several host threads (bench.py's CPU
+ * leg); the parity tests use the single-pass O2. */
+int orc_combine(int64_t G, const int32_t* kinds, int n_aggs, int64_t* rows_a, uint64_t* K_a,
+                int64_t* count_a, void* const* world_a, const int64_t* rows_b, const uint64_t* K_b,
+                const int64_t* count_b, void* const* world_b) {
+  int overflow = 0;
+  for (int64_t g = 0; g < G; g++) { rows_a[g] += rows_b[g]; K_a[g] |= K_b[g]; }
+  for (int a = 0; a < n_aggs; a++) {
+    if (!world_a[a]) continue;
+    for (int64_t cell = 0; cell < G * ORC_M; cell++) {
+      switch (kinds[a]) {
+        case K_SUM_I64: {
+          __int128 s = (__int128)((int64_t*)world_a[a])[cell] + ((const int64_t*)world_b[a])[cell];
+          if (s > (__int128)INT64_MAX || s < (__int128)INT64_MIN) overflow = 1;
+          ((int64_t*)world_a[a])[cell] = (int64_t)s;
+          break;
+        }
+        case K_SUM_F64:
+        case K_AVG_F64: ((double*)world_a[a])[cell] += ((const double*)world_b[a])[cell]; break;
+        case K_MIN_F64: {
+          double vb = ((const double*)world_b[a])[cell];
+          double* e = &((double*)world_a[a])[cell];
+          if (count_b[cell] > 0 && (count_a[cell] == 0 || tot_less(vb, *e))) *e = vb;
+          break;
+        }
+        case K_MAX_F64: {
+          double vb = ((const double*)world_b[a])[cell];
+          double* e = &((double*)world_a[a])[cell];
+          if (count_b[cell] > 0 && (count_a[cell] == 0 || tot_less(*e, vb))) *e = vb;
+          break;
+        }
+        default: break;
+      }
+    }
+  }
+  for (int64_t cell = 0; cell < G * ORC_M; cell++) count_a[cell] += count_b[cell];
   return overflow;
 }
 
@@ -326,6 +387,7 @@ int orc_agg_o1(const uint64_t* masks, int64_t n, const void* const* cols, const 
   __int128* is = (__int128*)malloc(sizeof(__int128) * (size_t)(G + 1));
   csum* fs = (csum*)malloc(sizeof(csum) * (size_t)(G + 1));
   double* ex = (double*)malloc(sizeof(double) * (size_t)(G + 1));
+  char* seen = (char*)malloc((size_t)(G + 1));
   for (int j = 0; j < ORC_M; j++) {
     /* COUNT(*) over I^(j) */
     for (int64_t g = 0; g < G; g++) cnt[g] = 0;
@@ -338,14 +400,22 @@ int orc_agg_o1(const uint64_t* masks, int64_t n, const void* const* cols, const 
       for (int64_t g = 0; g < G; g++) {
         is[g] = 0; fs[g].s = 0; fs[g].c = 0;
         ex[g] = (kind == K_MIN_F64) ? INFINITY : -INFINITY;
+        seen[g] = 0;
       }
       for (int64_t r = 0; r < n; r++) {
         if (gid[r] < 0 || !((masks[r] >> j) & 1u)) continue;
         int64_t g = gid[r];
         if (kind == K_SUM_I64) is[g] += (__int128)((const int64_t*)values[a])[r];
         else if (kind == K_SUM_F64 || kind == K_AVG_F64) csum_add(&fs[g], ((const double*)values[a])[r]);
-        else if (kind == K_MIN_F64) { double v = ((const double*)values[a])[r]; if (v < ex[g]) ex[g] = v; }
-        else if (kind == K_MAX_F64) { double v = ((const double*)values[a])[r]; if (v > ex[g]) ex[g] = v; }
+        else if (kind == K_MIN_F64) {  /* R31: the world's first value, then the total-order min */
+          double v = ((const double*)values[a])[r];
+          if (!seen[g] || tot_less(v, ex[g])) ex[g] = v;
+          seen[g] = 1;
+        } else if (kind == K_MAX_F64) {
+          double v = ((const double*)values[a])[r];
+          if (!seen[g] || tot_less(ex[g], v)) ex[g] = v;
+          seen[g] = 1;
+        }
       }
       for (int64_t g = 0; g < G; g++) {
         int64_t cell = g * ORC_M + j;
@@ -353,14 +423,14 @@ int orc_agg_o1(const uint64_t* masks, int64_t n, const void* const* cols, const 
           if (is[g] > (__int128)INT64_MAX || is[g] < (__int128)INT64_MIN) overflow = 1;
           ((int64_t*)world[a])[cell] = (int64_t)is[g];
         } else if (kind == K_SUM_F64 || kind == K_AVG_F64) {
-          ((double*)world[a])[cell] = fs[g].s + fs[g].c;
+          ((double*)world[a])[cell] = csum_value(&fs[g]);
         } else {
           ((double*)world[a])[cell] = ex[g];
         }
       }
     }
   }
-  free(gid); free(cnt); free(is); free(fs); free(ex);
+  free(gid); free(cnt); free(is); free(fs); free(ex); free(seen);
   return overflow;
 }
 
@@ -760,13 +830,13 @@ int orc_agg128(const uint64_t* masks, int64_t n, const void* const* cols, const 
           case K_MIN_F64: {
             double v = ((const double*)values[a])[r];
             double* e = &((double*)world[a])[cell];
-            if (v < *e) *e = v;
+            if (count[cell] == 1 || tot_less(v, *e)) *e = v;
             break;
           }
           case K_MAX_F64: {
             double v = ((const double*)values[a])[r];
             double* e = &((double*)world[a])[cell];
-            if (v > *e) *e = v;
+            if (count[cell] == 1 || tot_less(*e, v)) *e = v;
             break;
           }
           default: break;
@@ -782,7 +852,7 @@ int orc_agg128(const uint64_t* masks, int64_t n, const void* const* cols, const 
         if (v > (__int128)INT64_MAX || v < (__int128)INT64_MIN) overflow = 1;
         ((int64_t*)world[a])[cell] = (int64_t)v;
       } else if (kinds[a] == K_SUM_F64 || kinds[a] == K_AVG_F64) {
-        ((double*)world[a])[cell] = fsum[idx].s + fsum[idx].c;
+        ((double*)world[a])[cell] = csum_value(&fsum[idx]);
       }
     }
   }

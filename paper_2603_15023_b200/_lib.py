@@ -11,9 +11,9 @@ PAC_M = 64
 PAC_MAX_AGGS = 8
 PAC_MAX_KEYS = 4
 
-PAC_OK, PAC_E_INVAL, PAC_E_CAPACITY, PAC_E_WORKSPACE, PAC_E_CUDA, PAC_E_OVERFLOW = range(6)
+PAC_OK, PAC_E_INVAL, PAC_E_CAPACITY, PAC_E_WORKSPACE, PAC_E_CUDA, PAC_E_OVERFLOW, PAC_E_MERGE = range(7)
 STATUS_NAMES = {0: "PAC_OK", 1: "PAC_E_INVAL", 2: "PAC_E_CAPACITY", 3: "PAC_E_WORKSPACE",
-                4: "PAC_E_CUDA", 5: "PAC_E_OVERFLOW"}
+                4: "PAC_E_CUDA", 5: "PAC_E_OVERFLOW", 6: "PAC_E_MERGE"}
 
 COUNT, SUM_I64, SUM_F64, AVG_F64, MIN_F64, MAX_F64 = range(6)
 
@@ -103,6 +103,10 @@ def lib() -> ctypes.CDLL:
         "pac_launch_count": (ctypes.c_uint64, []),
         "pac_profile_enable": (ctypes.c_int, [ctypes.c_int]),
         "pac_profile_read": (ctypes.c_int, [_P, _P]),
+        "pac_profile_last_kernel": (ctypes.c_char_p, []),
+        "pac_merge_sizes": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int64, _P, _P, _P]),
+        "pac_merge_pack": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int64, _P, _P, _P, _P]),
+        "pac_merge_unpack": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int64, _P, _P, _P, _P]),
         "pac_version": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -127,4 +131,5 @@ def exported_symbols() -> list:
             "pac_lift", "pac_lift_cmp", "pac_noised_y_workspace_size", "pac_noised_y", "pac_cmp_index",
             "pac_select", "pac_select_cmp", "pac_filter", "pac_filter_cmp", "pac_join_table_bytes",
             "pac_join_build", "pac_join_table_status", "pac_join_mask", "pac_launch_count",
-            "pac_profile_enable", "pac_profile_read", "pac_version"]
+            "pac_profile_enable", "pac_profile_read", "pac_profile_last_kernel", "pac_version",
+            "pac_merge_sizes", "pac_merge_pack", "pac_merge_unpack"]

@@ -297,6 +297,36 @@ def remap(table: PacTable, union_keys: torch.Tensor, aggs) -> PacTable:
     return out
 
 
+class MergeBuffers:
+    """The three flat buffers of pac_merge_pack / pac_merge_unpack for tables of these kinds and
+    capacity: i64_sum (all_reduce SUM), f64_sum (SUM, may be empty), i64_min (MIN)."""
+
+    def __init__(self, kinds: Sequence[int], G_cap: int, device):
+        self.kinds = list(kinds)
+        self.G_cap = int(G_cap)
+        specs = _agg_specs([(k, None) for k in self.kinds])
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check("pac_merge_sizes", L.lib().pac_merge_sizes(specs, len(self.kinds), self.G_cap, ctypes.byref(a),
+                                                          ctypes.byref(b), ctypes.byref(c)))
+        self.i64_sum = torch.empty(a.value, dtype=torch.int64, device=device)
+        self.f64_sum = torch.empty(b.value, dtype=torch.float64, device=device)
+        self.i64_min = torch.empty(c.value, dtype=torch.int64, device=device)
+
+
+def merge_pack(table: PacTable, bufs: MergeBuffers) -> None:
+    specs = _agg_specs([(k, None) for k in table.kinds])
+    check("pac_merge_pack", L.lib().pac_merge_pack(
+        ctypes.byref(table.struct()), specs, len(table.kinds), bufs.G_cap, _ptr(bufs.i64_sum),
+        _ptr(bufs.f64_sum) if bufs.f64_sum.numel() else None, _ptr(bufs.i64_min), _stream(table.rows.device)))
+
+
+def merge_unpack(table: PacTable, bufs: MergeBuffers) -> None:
+    specs = _agg_specs([(k, None) for k in table.kinds])
+    check("pac_merge_unpack", L.lib().pac_merge_unpack(
+        ctypes.byref(table.struct()), specs, len(table.kinds), bufs.G_cap, _ptr(bufs.i64_sum),
+        _ptr(bufs.f64_sum) if bufs.f64_sum.numel() else None, _ptr(bufs.i64_min), _stream(table.rows.device)))
+
+
 # ------------------------------------------------------------------ finalize (a6, a7)
 class Finalizer:
     """pac_finalize with cached workspace/outputs."""
@@ -514,6 +544,10 @@ def profile_read() -> Tuple[float, int]:
     ms, n = ctypes.c_double(), ctypes.c_int64()
     check("pac_profile_read", L.lib().pac_profile_read(ctypes.byref(ms), ctypes.byref(n)))
     return float(ms.value), int(n.value)
+
+
+def profile_last_kernel() -> str:
+    return L.lib().pac_profile_last_kernel().decode()
 
 
 def version() -> str:

@@ -90,8 +90,8 @@ __global__ void __launch_bounds__(kThreads, PAC_MM_MINB) k_agg_minmax(AggPlan p,
   for (int i = tid; i < LH; i += nth) lstate[i] = 0;
   for (int i = tid; i < Lcap; i += nth) {
     lrows[i] = 0;
-    bmin[i] = kEncPosInf;   // nothing can be pruned until every world holds a value
-    bmax[i] = kEncNegInf;
+    bmin[i] = kMinEmpty;   // nothing can be pruned until every world holds a value
+    bmax[i] = kMaxEmpty;
   }
   for (int i = lane; i < nwords; i += 32) wdirty[i] = 0u;
   if (tid == 0) {
@@ -318,15 +318,15 @@ __global__ void __launch_bounds__(256) k_spill_agg(AggPlan p, const unsigned lon
     unsigned n0 = 0, n1 = 0;
     long long s0[NI > 0 ? NI : 1], s1[NI > 0 ? NI : 1];
     double f0[NF > 0 ? NF : 1], f1[NF > 0 ? NF : 1];
-    long long mn0 = kEncPosInf, mn1 = kEncPosInf, mx0 = kEncNegInf, mx1 = kEncNegInf;
+    long long mn0 = kMinEmpty, mn1 = kMinEmpty, mx0 = kMaxEmpty, mx1 = kMaxEmpty;
     auto reset = [&]() {
       n0 = n1 = 0;
 #pragma unroll
       for (int c = 0; c < NI; ++c) s0[c] = s1[c] = 0;
 #pragma unroll
       for (int c = 0; c < NF; ++c) f0[c] = f1[c] = 0.0;
-      mn0 = mn1 = kEncPosInf;
-      mx0 = mx1 = kEncNegInf;
+      mn0 = mn1 = kMinEmpty;
+      mx0 = mx1 = kMaxEmpty;
     };
     auto flush = [&]() {
       if (cur < 0) return;
@@ -345,10 +345,10 @@ __global__ void __launch_bounds__(256) k_spill_agg(AggPlan p, const unsigned lon
         if (n0) atomicAdd(&p.prov_fsum[c][b + lane], f0[c]);
         if (n1) atomicAdd(&p.prov_fsum[c][b + lane + 32], f1[c]);
       }
-      if ((MM & 1) && mn0 != kEncPosInf) atomicMin(&p.prov_min[b + lane], mn0);
-      if ((MM & 1) && mn1 != kEncPosInf) atomicMin(&p.prov_min[b + lane + 32], mn1);
-      if ((MM & 2) && mx0 != kEncNegInf) atomicMax(&p.prov_max[b + lane], mx0);
-      if ((MM & 2) && mx1 != kEncNegInf) atomicMax(&p.prov_max[b + lane + 32], mx1);
+      if ((MM & 1) && mn0 != kMinEmpty) atomicMin(&p.prov_min[b + lane], mn0);
+      if ((MM & 1) && mn1 != kMinEmpty) atomicMin(&p.prov_min[b + lane + 32], mn1);
+      if ((MM & 2) && mx0 != kMaxEmpty) atomicMax(&p.prov_max[b + lane], mx0);
+      if ((MM & 2) && mx1 != kMaxEmpty) atomicMax(&p.prov_max[b + lane + 32], mx1);
     };
     reset();
     for (int64_t b = c0; b < c1; b += 32) {
@@ -626,12 +626,12 @@ __global__ void k_gather(AggPlan p, const int* Gdev, const int* perm, pac_table 
     } else {
       bool a = false, b = false;
       if (p.has_max) {
-        a |= p.prov_max[pb + lane] != kEncNegInf;
-        b |= p.prov_max[pb + lane + 32] != kEncNegInf;
+        a |= p.prov_max[pb + lane] != kMaxEmpty;
+        b |= p.prov_max[pb + lane + 32] != kMaxEmpty;
       }
       if (p.has_min) {
-        a |= p.prov_min[pb + lane] != kEncPosInf;
-        b |= p.prov_min[pb + lane + 32] != kEncPosInf;
+        a |= p.prov_min[pb + lane] != kMinEmpty;
+        b |= p.prov_min[pb + lane + 32] != kMinEmpty;
       }
       K = (uint64_t)__ballot_sync(0xffffffffu, a) | ((uint64_t)__ballot_sync(0xffffffffu, b) << 32);
     }
@@ -643,8 +643,8 @@ __global__ void k_gather(AggPlan p, const int* Gdev, const int* perm, pac_table 
         const int j = lane + 32 * h;
         if (kd == 1) ((int64_t*)w)[ob + j] = (int64_t)p.prov_isum[ix][pb + j];
         else if (kd == 2) ((double*)w)[ob + j] = p.prov_fsum[ix][pb + j];
-        else if (kd == 3) ((double*)w)[ob + j] = dec_f64(p.prov_min[pb + j]);
-        else if (kd == 4) ((double*)w)[ob + j] = dec_f64(p.prov_max[pb + j]);
+        else if (kd == 3) ((double*)w)[ob + j] = dec_min(p.prov_min[pb + j]);
+        else if (kd == 4) ((double*)w)[ob + j] = dec_max(p.prov_max[pb + j]);
       }
     }
     if (lane == 0) {
@@ -1029,7 +1029,7 @@ static int device_info(int* sms, int* smem_optin) {
 }
 
 // profiling (runtime.cu)
-void profile_begin(cudaStream_t st);
+void profile_begin(cudaStream_t st, const char* name);
 void profile_end(cudaStream_t st);
 
 }  // namespace pac
@@ -1170,7 +1170,7 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
       per_sm = std::max(1, per_sm);
       int64_t tiles = (n_rows + kThreads * kMMRows - 1) / (kThreads * kMMRows);
       int grid = (int)std::min<int64_t>(tiles, (int64_t)sms * per_sm);
-      profile_begin(st);
+      profile_begin(st, "k_agg_minmax");
       k_agg_minmax<<<grid, kThreads, L.bytes, st>>>(p, L);
       note_launch();
       e = cudaGetLastError();
@@ -1225,9 +1225,11 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
         p.sp_cnt = (int*)(ws + S.o_cnt);
         if (cudaMemsetAsync(p.sp_cnt, 0, 4 * (size_t)G_cap, st) != cudaSuccess) return PAC_E_CUDA;
       }
-      profile_begin(st);
+      char kname[96];
+      snprintf(kname, sizeof(kname), "%s<%d,%d,%d>%s", L.tm ? "k_agg_tiles_tm" : "k_agg_tiles", A.ni, A.nf, mm,
+               S.cap > 0 ? " + k_spill_{resolve,offsets,scatter,agg}" : "");
+      profile_begin(st, kname);  // the timed region covers the whole aggregation pass
       e = L.tm ? kLaunchTm[A.ni][A.nf][mm](p, L, sms, st) : kLaunch[A.ni][A.nf][mm](p, L, sms, st);
-      profile_end(st);
       if (e == cudaSuccess && S.cap > 0) {
         unsigned long long* sp_tot = (unsigned long long*)(ws + W.o_ctr + 40);
         int* sp_off = (int*)(ws + S.o_off);
@@ -1240,6 +1242,7 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
         for (int q = 0; q < 4; ++q) note_launch();
         e = cudaGetLastError();
       }
+      profile_end(st);
     }
     if (e != cudaSuccess) return PAC_E_CUDA;
   }
@@ -1301,29 +1304,47 @@ extern "C" int pac_table_check(const pac_table* t, int64_t* h_num_groups, pac_st
 
 // ------------------------------------------------------------------ merge helpers (§8 a5/e)
 namespace pac {
-__global__ void k_rederive(pac_table t, int64_t G_cap, int has_count, int mm_a, int mm_kind) {
+// K after a cross-rank merge (NCCL has no OR).  With per-world counts K is exactly {j: count_j > 0}
+// (R5).  MIN/MAX-only tables carry no counts, and their double extremes cannot tell an empty world
+// from one holding only +inf (MIN) or -inf (MAX); there the caller merges the presence words
+// themselves (dist.py: MAX-allreduce of the 64 presence bits) and this kernel only adds the worlds
+// whose MIN or MAX is not the empty value -- it never clears a bit.
+__global__ void k_rederive(pac_table t, int64_t G_cap, int has_count, int min_a, int max_a) {
   const int64_t G = min(*t.d_num_groups, G_cap);
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   for (int64_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < G; g += (int64_t)gridDim.x * wpb) {
-    bool a, b;
+    bool a = false, b = false;
     if (has_count) {
       a = t.d_count[g * kM + lane] > 0;
       b = t.d_count[g * kM + lane + 32] > 0;
     } else {
-      const double* w = (const double*)t.d_world[mm_a];
-      const double s = mm_kind == PAC_MIN_F64 ? INFINITY : -INFINITY;
-      a = w[g * kM + lane] != s;
-      b = w[g * kM + lane + 32] != s;
+      const uint64_t K0 = t.d_presence[g];
+      a = (K0 >> lane) & 1ull;
+      b = (K0 >> (lane + 32)) & 1ull;
+      if (min_a >= 0) {
+        const double* w = (const double*)t.d_world[min_a];
+        a |= w[g * kM + lane] != INFINITY;
+        b |= w[g * kM + lane + 32] != INFINITY;
+      }
+      if (max_a >= 0) {
+        const double* w = (const double*)t.d_world[max_a];
+        a |= w[g * kM + lane] != -INFINITY;
+        b |= w[g * kM + lane + 32] != -INFINITY;
+      }
     }
     uint64_t K = (uint64_t)__ballot_sync(0xffffffffu, a) | ((uint64_t)__ballot_sync(0xffffffffu, b) << 32);
     if (lane == 0) t.d_presence[g] = K;
   }
 }
 
-__global__ void k_remap(pac_table in, const uint64_t* ukeys, int64_t Gu, pac_table out, int n_aggs,
-                        const int* kinds, int has_count) {
-  const int64_t Gin = *in.d_num_groups;
+struct RemapKinds {  // passed by value in the launch (no device buffer shared between calls)
+  int k[PAC_MAX_AGGS];
+};
+
+__global__ void k_remap(pac_table in, int64_t G_cap_in, const uint64_t* ukeys, int64_t Gu, pac_table out,
+                        int n_aggs, RemapKinds kinds, int has_count) {
+  const int64_t Gin = min(*in.d_num_groups, G_cap_in);  // a CAPACITY table holds G_cap_in groups
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   for (int64_t u = blockIdx.x * wpb + (threadIdx.x >> 5); u < Gu; u += (int64_t)gridDim.x * wpb) {
@@ -1338,7 +1359,7 @@ __global__ void k_remap(pac_table in, const uint64_t* ukeys, int64_t Gu, pac_tab
       const int j = lane + 32 * h;
       if (has_count) out.d_count[u * kM + j] = g >= 0 ? in.d_count[g * kM + j] : 0;
       for (int a = 0; a < n_aggs; ++a) {
-        const int k = kinds[a];
+        const int k = kinds.k[a];
         if (k == PAC_COUNT) continue;
         if (k == PAC_SUM_I64) {
           ((int64_t*)out.d_world[a])[u * kM + j] = g >= 0 ? ((const int64_t*)in.d_world[a])[g * kM + j] : 0;
@@ -1367,16 +1388,17 @@ extern "C" int pac_table_rederive_presence(const pac_table* t, const pac_agg_spe
   if (!t || G_cap < 1 || (t->m != 0 && t->m != 64)) return PAC_E_INVAL;  // m = 64 tables
   int rc = build_accs(aggs, n_aggs, &A, true, true);  // only the kinds matter here
   if (rc) return rc;
-  int mm_a = -1, mm_kind = 0;
-  for (int a = 0; a < n_aggs; ++a)
-    if (aggs[a].kind == PAC_MIN_F64 || aggs[a].kind == PAC_MAX_F64) {
-      mm_a = a;
-      mm_kind = aggs[a].kind;
-      break;
-    }
-  if (A.has_count ? !t->d_count : (mm_a < 0 || !t->d_world[mm_a])) return PAC_E_INVAL;
+  int min_a = -1, max_a = -1;
+  for (int a = 0; a < n_aggs; ++a) {
+    if (aggs[a].kind == PAC_MIN_F64 && min_a < 0) min_a = a;
+    if (aggs[a].kind == PAC_MAX_F64 && max_a < 0) max_a = a;
+  }
+  if (A.has_count ? !t->d_count : ((min_a < 0 || !t->d_world[min_a]) && (max_a < 0 || !t->d_world[max_a])))
+    return PAC_E_INVAL;
+  if (min_a >= 0 && !t->d_world[min_a]) min_a = -1;
+  if (max_a >= 0 && !t->d_world[max_a]) max_a = -1;
   int blocks = (int)std::min<int64_t>((G_cap + 7) / 8, 148 * 16);
-  k_rederive<<<std::max(1, blocks), 256, 0, (cudaStream_t)stream>>>(*t, G_cap, A.has_count, mm_a, mm_kind);
+  k_rederive<<<std::max(1, blocks), 256, 0, (cudaStream_t)stream>>>(*t, G_cap, A.has_count, min_a, max_a);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
@@ -1389,15 +1411,11 @@ extern "C" int pac_table_remap(const pac_table* in, const uint64_t* d_union_keys
   if ((in->m != 0 && in->m != 64) || (out->m != 0 && out->m != 64)) return PAC_E_INVAL;  // m = 64 tables
   int rc = build_accs(aggs, n_aggs, &A, true, true);  // only the kinds matter here
   if (rc) return rc;
-  // kinds are passed by value through a small device buffer embedded in the launch
-  static int* d_kinds = nullptr;
-  if (!d_kinds && cudaMalloc(&d_kinds, sizeof(int) * PAC_MAX_AGGS) != cudaSuccess) return PAC_E_CUDA;
-  int hk[PAC_MAX_AGGS] = {0};
-  for (int a = 0; a < n_aggs; ++a) hk[a] = aggs[a].kind;
+  RemapKinds hk{};
+  for (int a = 0; a < n_aggs; ++a) hk.k[a] = aggs[a].kind;
   cudaStream_t st = (cudaStream_t)stream;
-  if (cudaMemcpyAsync(d_kinds, hk, sizeof(hk), cudaMemcpyHostToDevice, st) != cudaSuccess) return PAC_E_CUDA;
   int blocks = (int)std::min<int64_t>((G_union + 7) / 8, 148 * 16);
-  k_remap<<<std::max(1, blocks), 256, 0, st>>>(*in, d_union_keys, G_union, *out, n_aggs, d_kinds, A.has_count);
+  k_remap<<<std::max(1, blocks), 256, 0, st>>>(*in, G_cap_in, d_union_keys, G_union, *out, n_aggs, hk, A.has_count);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }

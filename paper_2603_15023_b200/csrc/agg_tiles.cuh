@@ -163,8 +163,8 @@ __device__ __forceinline__ void init_prov_slot(const AggPlan& p, int prov, uint6
   if (p.has_count) fill_world_row(p.prov_count + b, 0);
   for (int c = 0; c < p.ni; ++c) fill_world_row(p.prov_isum[c] + b, 0);
   for (int c = 0; c < p.nf; ++c) fill_world_row(p.prov_fsum[c] + b, 0);  // +0.0
-  if (p.has_min) fill_world_row(p.prov_min + b, kEncPosInf);
-  if (p.has_max) fill_world_row(p.prov_max + b, kEncNegInf);
+  if (p.has_min) fill_world_row(p.prov_min + b, kMinEmpty);
+  if (p.has_max) fill_world_row(p.prov_max + b, kMaxEmpty);
 }
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* a) {
@@ -384,7 +384,7 @@ struct WarpAcc {
   unsigned c0, c1;
   long long ia0[NI > 0 ? NI : 1], ia1[NI > 0 ? NI : 1];
   double fa0[NF > 0 ? NF : 1], fa1[NF > 0 ? NF : 1];
-  double mn0, mn1, mx0, mx1;
+  long long mn0, mn1, mx0, mx1;  // enc_f64 extremes (R31 total order), kMinEmpty / kMaxEmpty when empty
 
   __device__ __forceinline__ void reset() {
     c0 = c1 = 0;
@@ -392,8 +392,8 @@ struct WarpAcc {
     for (int c = 0; c < NI; ++c) ia0[c] = ia1[c] = 0;
 #pragma unroll
     for (int c = 0; c < NF; ++c) fa0[c] = fa1[c] = 0.0;
-    mn0 = mn1 = INFINITY;
-    mx0 = mx1 = -INFINITY;
+    mn0 = mn1 = kMinEmpty;
+    mx0 = mx1 = kMaxEmpty;
   }
   // add into the CTA's smem table (shared by the warps working on the same slot)
   __device__ __forceinline__ void flush(unsigned* cnt, unsigned long long* isum, double* fsum, long long* emin,
@@ -413,12 +413,12 @@ struct WarpAcc {
       if (fa1[c] != 0.0) atomicAdd(&fsum[(size_t)c * Lcap * kM + b + lane + 32], fa1[c]);
     }
     if (MM & 1) {
-      atomicMin(&emin[b + lane], enc_f64(mn0));
-      atomicMin(&emin[b + lane + 32], enc_f64(mn1));
+      if (mn0 != kMinEmpty) atomicMin(&emin[b + lane], mn0);
+      if (mn1 != kMinEmpty) atomicMin(&emin[b + lane + 32], mn1);
     }
     if (MM & 2) {
-      atomicMax(&emax[b + lane], enc_f64(mx0));
-      atomicMax(&emax[b + lane + 32], enc_f64(mx1));
+      if (mx0 != kMaxEmpty) atomicMax(&emax[b + lane], mx0);
+      if (mx1 != kMaxEmpty) atomicMax(&emax[b + lane + 32], mx1);
     }
     reset();
   }
@@ -433,7 +433,7 @@ struct RunCtx {  // read-only per-tile state of phase C
   const unsigned long long* smask;
   const long long* sival;
   const double* sfval;
-  const double* smval;
+  const long long* smval;
   const uint32_t* rdesc;
   const uint4* xcs;
   const uint2* xcs2;
@@ -450,7 +450,7 @@ template <int NI, int NF, int MM, bool GENERIC>
 __device__ __forceinline__ void run_body(WarpAcc<NI, NF, MM>& acc, const unsigned long long* __restrict__ smask,
                                          const long long* __restrict__ sival, int istride,
                                          const double* __restrict__ sfval, int fstride,
-                                         const double* __restrict__ smval, int len, const XposeConst& xc, int lane,
+                                         const long long* __restrict__ smval, int len, const XposeConst& xc, int lane,
                                          bool small_rt = true, bool fin_rt = true) {
   // GENERIC = false: the common case (SMALL and FIN) with no runtime tests inside the loop
   const bool SMALL = GENERIC ? small_rt : true;
@@ -509,24 +509,25 @@ __device__ __forceinline__ void run_body(WarpAcc<NI, NF, MM>& acc, const unsigne
       acc.fa1[c] += shfl_d(t, a1);
       acc.fa1[c] += shfl_d(t, b1);
     }
-    if (MM) {
-      const double2 u = *(const double2*)(smval + row);
-      const double2 w = *(const double2*)(smval + row + 2);
+    if (MM) {  // extremes on enc_f64 encodings (R31 total order: NaN above +inf); the
+               // empty subset is the sentinel, which every encoded value beats
+      const longlong2 u = *(const longlong2*)(smval + row);
+      const longlong2 w = *(const longlong2*)(smval + row + 2);
       if (MM & 1) {
-        double t = ib0 ? u.x : INFINITY;
-        if (ib1) t = fmin(t, u.y);
-        if (ib2) t = fmin(t, w.x);
-        if (ib3) t = fmin(t, w.y);
-        acc.mn0 = fmin(acc.mn0, fmin(shfl_d(t, a0), shfl_d(t, b0)));
-        acc.mn1 = fmin(acc.mn1, fmin(shfl_d(t, a1), shfl_d(t, b1)));
+        long long t = ib0 ? u.x : kMinEmpty;
+        if (ib1) t = min(t, u.y);
+        if (ib2) t = min(t, w.x);
+        if (ib3) t = min(t, w.y);
+        acc.mn0 = min(acc.mn0, min(__shfl_sync(0xffffffffu, t, a0), __shfl_sync(0xffffffffu, t, b0)));
+        acc.mn1 = min(acc.mn1, min(__shfl_sync(0xffffffffu, t, a1), __shfl_sync(0xffffffffu, t, b1)));
       }
       if (MM & 2) {
-        double t = ib0 ? u.x : -INFINITY;
-        if (ib1) t = fmax(t, u.y);
-        if (ib2) t = fmax(t, w.x);
-        if (ib3) t = fmax(t, w.y);
-        acc.mx0 = fmax(acc.mx0, fmax(shfl_d(t, a0), shfl_d(t, b0)));
-        acc.mx1 = fmax(acc.mx1, fmax(shfl_d(t, a1), shfl_d(t, b1)));
+        long long t = ib0 ? u.x : kMaxEmpty;
+        if (ib1) t = max(t, u.y);
+        if (ib2) t = max(t, w.x);
+        if (ib3) t = max(t, w.y);
+        acc.mx0 = max(acc.mx0, max(__shfl_sync(0xffffffffu, t, a0), __shfl_sync(0xffffffffu, t, b0)));
+        acc.mx1 = max(acc.mx1, max(__shfl_sync(0xffffffffu, t, a1), __shfl_sync(0xffffffffu, t, b1)));
       }
     }
   }
@@ -577,7 +578,7 @@ struct TileSmem {
   long long* sival;           // [NI][TS]
   uint32_t* rdesc;            // [runs] run descriptors (pack_run)
   double* sfval;              // [NF][TS]
-  double* smval;              // [TS]
+  long long* smval;           // [TS] enc_f64 of the MIN/MAX column
   unsigned short* sslot;      // [T]
   unsigned char* srank;       // [T]
   unsigned short* ucnt;       // [units][Lcap]
@@ -839,7 +840,7 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
         for (int c = 0; c < NI; ++c) sm.sival[c * TS + q] = 0;
 #pragma unroll
         for (int c = 0; c < NF; ++c) sm.sfval[c * TS + q] = 0.0;
-        if (MM) sm.smval[q] = 0.0;
+        if (MM) sm.smval[q] = 0;
       }
       for (int i = lane; 32 * i < hs; i += 32) sm.rdesc[rb + i] = pack_run(o0 + 32 * i, s, min(32, hs - 32 * i));
       if (lane == 0) sm.lrows[s] += (unsigned long long)hs;
@@ -899,7 +900,7 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
       for (int c = 0; c < NI; ++c) sm.sival[c * TS + q] = 0;
 #pragma unroll
       for (int c = 0; c < NF; ++c) sm.sfval[c * TS + q] = 0.0;
-      if (MM) sm.smval[q] = 0.0;
+      if (MM) sm.smval[q] = 0;
     }
     for (int i = 0, rb = sm.runoffs[s]; 32 * i < h; ++i)
       sm.rdesc[rb + i] = pack_run(o0 + 32 * i, s, min(32, h - 32 * i));
@@ -958,7 +959,7 @@ __device__ __forceinline__ void tile_mid(const AggPlan& p, const TileSmem& sm, c
         emax = max(emax, (uint32_t)__double2hiint(v) & 0x7FF00000u);
         sm.sfval[c * TS + pos] = v;
       }
-      if (MM) sm.smval[pos] = __longlong_as_double((long long)tc.w8(KM, li));
+      if (MM) sm.smval[pos] = enc_f64(__longlong_as_double((long long)tc.w8(KM, li)));
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -1015,7 +1016,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
   sm.sival = (long long*)(smem + L.o_ival);
   sm.rdesc = (uint32_t*)(smem + L.o_rdesc);
   sm.sfval = (double*)(smem + L.o_fval);
-  sm.smval = (double*)(smem + L.o_mval);
+  sm.smval = (long long*)(smem + L.o_mval);
   sm.sslot = (unsigned short*)(smem + L.o_slot);
   sm.srank = (unsigned char*)(smem + L.o_rank);
   sm.ucnt = (unsigned short*)(smem + L.o_ucnt);
@@ -1047,8 +1048,8 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? PAC_TILE_MINB : 1) k
     for (int c = 0; c < NI; ++c) sm.isum[(size_t)c * Lcap * kM + i] = 0;
 #pragma unroll
     for (int c = 0; c < NF; ++c) sm.fsum[(size_t)c * Lcap * kM + i] = 0.0;
-    if (MM & 1) sm.emin[i] = kEncPosInf;
-    if (MM & 2) sm.emax[i] = kEncNegInf;
+    if (MM & 1) sm.emin[i] = kMinEmpty;
+    if (MM & 2) sm.emax[i] = kMaxEmpty;
   }
   if (tid == 0) {
     misc->nlocal = 0;

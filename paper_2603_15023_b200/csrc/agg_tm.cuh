@@ -64,11 +64,11 @@ __device__ __forceinline__ void tm_init_slot(uint32_t a) {
 #pragma unroll
   for (int c = 0; c < NF; ++c) tm_st4(a + S::o_fsum + 4 * c, 0u, 0u, 0u, 0u);
   if (MM & 1) {
-    const uint64_t e = (uint64_t)kEncPosInf;
+    const uint64_t e = (uint64_t)kMinEmpty;
     tm_st4(a + S::o_min, (uint32_t)e, (uint32_t)(e >> 32), (uint32_t)e, (uint32_t)(e >> 32));
   }
   if (MM & 2) {
-    const uint64_t e = (uint64_t)kEncNegInf;
+    const uint64_t e = (uint64_t)kMaxEmpty;
     tm_st4(a + S::o_max, (uint32_t)e, (uint32_t)(e >> 32), (uint32_t)e, (uint32_t)(e >> 32));
   }
 }
@@ -101,13 +101,13 @@ __device__ __forceinline__ void tm_flush(const WarpAcc<NI, NF, MM>& acc, uint32_
     tm_st4(a + S::o_fsum + 4 * c, (uint32_t)b0, (uint32_t)(b0 >> 32), (uint32_t)b1, (uint32_t)(b1 >> 32));
   }
   if (MM & 1) {
-    const long long e0 = min((long long)u64of(mn[0], mn[1]), enc_f64(acc.mn0));
-    const long long e1 = min((long long)u64of(mn[2], mn[3]), enc_f64(acc.mn1));
+    const long long e0 = min((long long)u64of(mn[0], mn[1]), acc.mn0);
+    const long long e1 = min((long long)u64of(mn[2], mn[3]), acc.mn1);
     tm_st4(a + S::o_min, (uint32_t)e0, (uint32_t)((uint64_t)e0 >> 32), (uint32_t)e1, (uint32_t)((uint64_t)e1 >> 32));
   }
   if (MM & 2) {
-    const long long e0 = max((long long)u64of(mx[0], mx[1]), enc_f64(acc.mx0));
-    const long long e1 = max((long long)u64of(mx[2], mx[3]), enc_f64(acc.mx1));
+    const long long e0 = max((long long)u64of(mx[0], mx[1]), acc.mx0);
+    const long long e1 = max((long long)u64of(mx[2], mx[3]), acc.mx1);
     tm_st4(a + S::o_max, (uint32_t)e0, (uint32_t)((uint64_t)e0 >> 32), (uint32_t)e1, (uint32_t)((uint64_t)e1 >> 32));
   }
   tm_wait_st();
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_agg_tiles_tm(AggPlan p, SmemL
   sm.sival = (long long*)(smem + L.o_ival);
   sm.rdesc = (uint32_t*)(smem + L.o_rdesc);
   sm.sfval = (double*)(smem + L.o_fval);
-  sm.smval = (double*)(smem + L.o_mval);
+  sm.smval = (long long*)(smem + L.o_mval);
   sm.sslot = (unsigned short*)(smem + L.o_slot);
   sm.srank = (unsigned char*)(smem + L.o_rank);
   sm.ucnt = (unsigned short*)(smem + L.o_ucnt);

@@ -1,5 +1,6 @@
 // Device helpers shared by the libpac kernels (product side; independent of oracle/).
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <cuda_runtime.h>
@@ -143,7 +144,15 @@ __host__ __device__ __forceinline__ u32x4 philox4x32_10(u32x4 c, uint32_t k0, ui
 enum { kTagCell = 0, kTagJstar = 1, kTagSalt = 2, kTagLift = 3, kTagFilter = 4 };  // R13, R24, R25
 
 // ------------------------------------------------------------------ ordered f64 <-> int64
-// Monotone map of doubles onto signed int64, so MIN/MAX become atomicMin/atomicMax.
+// Monotone map of doubles onto signed int64 under the total order of R31 (DuckDB's order on
+// DOUBLE: IEEE order, every NaN equal and larger than +inf), so MIN/MAX become integer
+// min/max and atomicMin/atomicMax.  Every NaN maps to kEncNaN (just above enc(+inf)).  The
+// empty-world sentinels kMinEmpty / kMaxEmpty lie outside the range of every encoded value,
+// so "world present" == "extreme != sentinel" holds exactly (a world holding only +inf under
+// MIN, or only NaN, is present).
+constexpr long long kEncNaN = 0x7FF8000000000000ll;
+constexpr long long kMinEmpty = 0x7FFFFFFFFFFFFFFFll;            // empty MIN world
+constexpr long long kMaxEmpty = (long long)0x8000000000000000ull;  // empty MAX world
 __host__ __device__ __forceinline__ long long enc_f64(double v) {
 #ifdef __CUDA_ARCH__
   long long i = __double_as_longlong(v);
@@ -151,6 +160,7 @@ __host__ __device__ __forceinline__ long long enc_f64(double v) {
   long long i;
   memcpy(&i, &v, 8);
 #endif
+  if ((i & 0x7FFFFFFFFFFFFFFFll) > 0x7FF0000000000000ll) return kEncNaN;
   return i >= 0 ? i : (i ^ 0x7FFFFFFFFFFFFFFFll);
 }
 __host__ __device__ __forceinline__ double dec_f64(long long i) {
@@ -163,8 +173,9 @@ __host__ __device__ __forceinline__ double dec_f64(long long i) {
   return v;
 #endif
 }
-constexpr long long kEncPosInf = 0x7FF0000000000000ll;                 // enc(+inf)
-constexpr long long kEncNegInf = (long long)0x800FFFFFFFFFFFFFull;     // enc(-inf)
+// table value of an encoded extreme: an empty world reads +inf (MIN) / -inf (MAX)
+__host__ __device__ __forceinline__ double dec_min(long long e) { return e == kMinEmpty ? INFINITY : dec_f64(e); }
+__host__ __device__ __forceinline__ double dec_max(long long e) { return e == kMaxEmpty ? -INFINITY : dec_f64(e); }
 
 // ------------------------------------------------------------------ group keys (R20)
 __device__ __forceinline__ uint64_t load_key_part(const void* col, int w, int64_t row) {

@@ -1,6 +1,7 @@
 // libpac runtime: launch accounting, kernel timing hooks, version.
 #include <atomic>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -12,12 +13,14 @@ static std::atomic<int> g_profile{0};
 static std::mutex g_mu;
 static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
 static cudaEvent_t g_pending = nullptr;
+static std::string g_name;  // kernel(s) of the last timed region
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-void profile_begin(cudaStream_t st) {
+void profile_begin(cudaStream_t st, const char* name) {
   if (!g_profile.load()) return;
   std::lock_guard<std::mutex> lk(g_mu);
+  g_name = name ? name : "";
   cudaEvent_t a;
   if (cudaEventCreate(&a) != cudaSuccess) return;
   cudaEventRecord(a, st);
@@ -64,4 +67,11 @@ extern "C" int pac_profile_read(double* h_total_ms, int64_t* h_launches) {
   return rc;
 }
 
-extern "C" const char* pac_version(void) { return "libpac 0.1.0 (sm_100a)"; }
+extern "C" const char* pac_profile_last_kernel(void) {
+  std::lock_guard<std::mutex> lk(pac::g_mu);
+  static thread_local std::string copy;
+  copy = pac::g_name;
+  return copy.c_str();
+}
+
+extern "C" const char* pac_version(void) { return "libpac 0.2.0 (sm_100a)"; }

@@ -95,6 +95,7 @@ struct FinPrep {
   double* zbuf;     // [cells]
   uint8_t* is_null; // [cells]
   uint8_t* flags;   // [G]
+  const int32_t* status;  // the table's status (pac_finalize) or NULL
 };
 
 // one thread per cell: Philox block, NULL decision, normal draw, diversity flag (the y-vectors are
@@ -113,10 +114,14 @@ __global__ void k_finalize_prep(FinPrep f) {
     for (int w = 0; w < W; ++w) pc += __popcll(f.K[g * W + w]);
     const u32x4 x = philox4x32_10({(uint32_t)cell, (uint32_t)((uint64_t)cell >> 32), f.round, kTagCell},
                                   (uint32_t)f.seed, (uint32_t)(f.seed >> 32));
-    const bool null = (int)(x.x >> (M == 64 ? 26 : 25)) >= pc;  // R10 / R29
+    // a table with a nonzero status (CAPACITY: groups missing; OVERFLOW: a wrapped int64 sum)
+    // releases nothing: every cell NULL, flags bit 1, the posterior untouched
+    const bool bad = f.status && *f.status != 0;
+    const bool null = bad || (int)(x.x >> (M == 64 ? 26 : 25)) >= pc;  // R10 / R29
     f.is_null[cell] = null ? 1 : 0;
     f.zbuf[cell] = null ? 0.0 : normal_from(x);
-    if (a == 0 && f.flags) f.flags[g] = (f.rows[g] >= M && pc <= (M == 64 ? 34 : 68)) ? 1 : 0;  // R18 / R29
+    if (a == 0 && f.flags)
+      f.flags[g] = (uint8_t)(((f.rows[g] >= M && pc <= (M == 64 ? 34 : 68)) ? 1 : 0) | (bad ? 2 : 0));  // R18 / R29
   }
 }
 
@@ -531,6 +536,8 @@ extern "C" int pac_session_query(const pac_session* s, uint64_t* salt, int32_t* 
 
 extern "C" int pac_session_set_posterior(pac_session* s, const double* h_P64) {
   if (!s || !h_P64) return PAC_E_INVAL;
+  // a finalize chain still running on a (non-blocking) stream reads and writes d_P: wait for it
+  if (cudaDeviceSynchronize() != cudaSuccess) return PAC_E_CUDA;
   if (cudaMemcpy(s->d_P, h_P64, s->m * 8, cudaMemcpyHostToDevice) != cudaSuccess) return PAC_E_CUDA;
   return cudaDeviceSynchronize() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
@@ -577,6 +584,7 @@ extern "C" int pac_finalize(pac_session* s, const pac_table* t, const pac_agg_sp
   f.zbuf = (double*)(ws + oz);
   f.is_null = d_is_null;
   f.flags = d_flags;
+  f.status = t->d_status;
   YSrc ys{};
   for (int a = 0; a < n_aggs; ++a) {
     ys.kinds[a] = aggs[a].kind;

@@ -1,23 +1,29 @@
 """Row-sharded multi-GPU merge (the paper's analogue is DuckDB's thread-local
 partial aggregates + state.combine).
 
-Each rank aggregates its contiguous row shard with the same salt, then the partial
-64-world tables are merged over NCCL (NVLink / NVSwitch):
-  1. union dictionary: all ranks allgather their group keys; the sorted union is the common
-     layout (skipped when every rank already has the same keys, e.g. dense group domains);
-  2. libpac remaps each table onto the union layout (pac_table_remap);
-  3. one coalesced set of all_reduce calls: SUM on int64 {rows, count, SUM_I64 worlds} and
-     f64 {SUM_F64 / AVG_F64 worlds}, MIN / MAX on the f64 extremes;
-  4. NCCL has no bitwise-OR reduction, so K is re-derived on the device from the merged
-     counts or extremes (pac_table_rederive_presence).
+Each rank aggregates its contiguous row shard with the same salt, then the partial 64-world
+tables are merged over NCCL (NVLink / NVSwitch):
+  1. common layout: every rank's table must sit on one group dictionary.  Dense domains
+     (every rank holds every group, e.g. BASELINE C5's 100 groups) already do -- pass
+     `same_keys=True` and nothing is exchanged or synchronised for it; the dictionary
+     fingerprint that travels with the data catches a wrong claim on the device
+     (PAC_E_MERGE in the table status).  Otherwise the ranks allgather their keys, take the
+     sorted union and libpac remaps each table onto it (pac_table_remap) -- host syncs, the
+     general path;
+  2. libpac packs the table into three flat buffers (pac_merge_pack);
+  3. three all_reduce calls, issued back to back: SUM on the int64 buffer {rows, counts,
+     SUM_I64 worlds}, SUM on the f64 buffer {SUM_F64 / AVG_F64 worlds}, MIN on the int64
+     buffer {fingerprint, status, order-preserving MIN encodings, bit-inverted MAX encodings};
+  4. libpac unpacks into the table (pac_merge_unpack): K from the merged counts, or for
+     MIN/MAX-only tables from the merged extremes (NCCL has no OR; the encoding carries it).
 Finalize then runs identically on every rank (same table, same session seed).
 
-The communication helpers work on any torch.distributed backend (NCCL on the GPU box,
-gloo in the CPU tests); they only move tensors -- no method arithmetic here.
+The communication helpers work on any torch.distributed backend (NCCL on the GPU box, gloo in
+the CPU tests); they only move tensors -- no method arithmetic here.
 """
 from __future__ import annotations
 
-from typing import Dict, List, Sequence, Tuple
+from typing import Optional, Sequence, Tuple
 
 import torch
 import torch.distributed as dist
@@ -25,8 +31,8 @@ import torch.distributed as dist
 from ._lib import AVG_F64, COUNT, MAX_F64, MIN_F64, SUM_F64, SUM_I64
 
 
-def reduce_ops_for(kinds: Sequence[int]) -> List[str]:
-    """all_reduce op per world array of a table with these aggregate kinds."""
+def reduce_ops_for(kinds: Sequence[int]):
+    """The reduction each aggregate's world array takes in the merge (documentation / tests)."""
     ops = []
     for k in kinds:
         if k == COUNT:
@@ -42,13 +48,10 @@ def reduce_ops_for(kinds: Sequence[int]) -> List[str]:
     return ops
 
 
-_OPS = {"sum": dist.ReduceOp.SUM, "min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}
-
-
 def union_keys(local_keys: torch.Tensor, group=None) -> Tuple[torch.Tensor, bool]:
     """Sorted union (as unsigned 64-bit order) of every rank's group keys (int64 bit
     patterns).  Returns (union, same) where `same` is True when every rank already holds
-    exactly the union (no remap needed)."""
+    exactly the union (no remap needed).  Synchronises with the host (sizes)."""
     ws = dist.get_world_size(group)
     n = torch.tensor([local_keys.numel()], dtype=torch.int64, device=local_keys.device)
     sizes = [torch.zeros_like(n) for _ in range(ws)]
@@ -71,28 +74,39 @@ def union_keys(local_keys: torch.Tensor, group=None) -> Tuple[torch.Tensor, bool
     return u, bool(f.item())
 
 
-def allreduce_table_tensors(rows: torch.Tensor, count, worlds: Sequence, kinds: Sequence[int],
-                            group=None) -> None:
-    """In-place merge of one table laid out on the common dictionary."""
-    dist.all_reduce(rows, op=dist.ReduceOp.SUM, group=group)
-    if count is not None:
-        dist.all_reduce(count, op=dist.ReduceOp.SUM, group=group)
-    for w, op in zip(worlds, reduce_ops_for(kinds)):
-        if w is None or op == "none":
-            continue
-        dist.all_reduce(w, op=_OPS[op], group=group)
+def merge_flat(i64_sum: torch.Tensor, f64_sum: torch.Tensor, i64_min: torch.Tensor, group=None) -> None:
+    """The three reductions of the flat merge buffers (in place, issued back to back)."""
+    works = [dist.all_reduce(i64_sum, op=dist.ReduceOp.SUM, group=group, async_op=True)]
+    if f64_sum.numel():
+        works.append(dist.all_reduce(f64_sum, op=dist.ReduceOp.SUM, group=group, async_op=True))
+    works.append(dist.all_reduce(i64_min, op=dist.ReduceOp.MIN, group=group, async_op=True))
+    for w in works:
+        w.wait()
 
 
-def merge_table(table, aggs, group=None):
-    """Merge a libpac PacTable across the process group; returns the merged table (the
-    input table itself when no remap was needed)."""
+_BUFS = {}
+
+
+def merge_table(table, aggs, group=None, same_keys: bool = False, bufs=None):
+    """Merge a libpac PacTable across the process group; returns the merged table (the input
+    table itself unless a remap onto the union dictionary was needed).
+
+    same_keys=True: the caller asserts every rank's table already has the same groups in the
+    same order (dense domains); then the merge is pack + three all_reduce + unpack with no
+    host synchronisation, and a wrong assertion ends in PAC_E_MERGE in the table status."""
     from . import api
-    G = table.check()
-    keys = table.group_key[:G]
-    u, same = union_keys(keys, group)
-    t = table if same else api.remap(table, u, aggs)
-    Gu = u.numel()
-    worlds = [None if w is None else w[:Gu] for w in t.world]
-    allreduce_table_tensors(t.rows[:Gu], None if t.count is None else t.count[:Gu], worlds, t.kinds, group)
-    api.rederive_presence(t, aggs)
+    t = table
+    if not same_keys:
+        G = table.check()
+        u, same = union_keys(table.group_key[:G], group)
+        if not same:
+            t = api.remap(table, u, aggs)
+    if bufs is None:
+        key = (tuple(t.kinds), t.G_cap, str(t.rows.device))
+        bufs = _BUFS.get(key)
+        if bufs is None:
+            bufs = _BUFS[key] = api.MergeBuffers(t.kinds, t.G_cap, t.rows.device)
+    api.merge_pack(t, bufs)
+    merge_flat(bufs.i64_sum, bufs.f64_sum, bufs.i64_min, group)
+    api.merge_unpack(t, bufs)
     return t

@@ -42,8 +42,69 @@ def _aggs(iv, fv):
     return [(k, vals[k]) for k in KINDS]
 
 
+MIN_EMPTY = np.int64(0x7FFFFFFFFFFFFFFF)
+MAX_EMPTY = np.int64(-0x8000000000000000)
+
+
+def _enc(v):
+    """include/pac.h's order-preserving encoding (R31): NaN -> one value above +inf."""
+    b = np.ascontiguousarray(v, dtype=np.float64).view(np.int64).copy()
+    nan = np.isnan(v)
+    b = np.where(b >= 0, b, b ^ np.int64(0x7FFFFFFFFFFFFFFF))
+    return np.where(nan, np.int64(0x7FF8000000000000), b)
+
+
+def _dec(e):
+    b = np.where(e >= 0, e, e ^ np.int64(0x7FFFFFFFFFFFFFFF))
+    return b.view(np.float64)
+
+
+def _pack(G, rows, count, worlds, K):
+    """The flat-buffer layout of include/pac.h (pac_merge_pack), written from the header:
+    i64_sum = rows | count | SUM_I64 worlds; f64_sum = SUM/AVG worlds; i64_min = f, ~f,
+    ~status, MIN encodings, ~MAX encodings (sentinel for worlds outside K)."""
+    Kb = ((K[:, None] >> np.arange(64, dtype=np.uint64)) & np.uint64(1)).astype(bool)
+    i64 = [rows, count.ravel()]
+    f64, mn = [], [np.array([12345, ~12345, ~0], dtype=np.int64)]
+    for a, k in enumerate(KINDS):
+        if k == dg.AGG_SUM_I64:
+            i64.append(worlds[a].ravel())
+        elif k in (dg.AGG_SUM_F64, dg.AGG_AVG_F64):
+            f64.append(worlds[a].ravel())
+        elif k == dg.AGG_MIN_F64:
+            mn.append(np.where(Kb, _enc(worlds[a]), MIN_EMPTY).ravel())
+        elif k == dg.AGG_MAX_F64:
+            mn.append(~np.where(Kb, _enc(worlds[a]), MAX_EMPTY).ravel())
+    return (torch.from_numpy(np.concatenate(i64).astype(np.int64)), torch.from_numpy(np.concatenate(f64)),
+            torch.from_numpy(np.concatenate(mn).astype(np.int64)))
+
+
+def _unpack(G, i64, f64, mn):
+    i64, f64, mn = i64.numpy(), f64.numpy(), mn.numpy()
+    rows, count = i64[:G], i64[G:G + 64 * G].reshape(G, 64)
+    oi, of, om = G + 64 * G, 0, 3
+    worlds = []
+    for k in KINDS:
+        if k == dg.AGG_COUNT:
+            worlds.append(None)
+        elif k == dg.AGG_SUM_I64:
+            worlds.append(i64[oi:oi + 64 * G].reshape(G, 64)); oi += 64 * G
+        elif k in (dg.AGG_SUM_F64, dg.AGG_AVG_F64):
+            worlds.append(f64[of:of + 64 * G].reshape(G, 64)); of += 64 * G
+        elif k == dg.AGG_MIN_F64:
+            e = mn[om:om + 64 * G].reshape(G, 64); om += 64 * G
+            worlds.append(np.where(e == MIN_EMPTY, np.inf, _dec(e)))
+        else:
+            e = ~mn[om:om + 64 * G].reshape(G, 64); om += 64 * G
+            worlds.append(np.where(e == MAX_EMPTY, -np.inf, _dec(e)))
+    assert mn[0] == ~mn[1]  # every rank packed the same dictionary fingerprint
+    return rows, count, worlds
+
+
 def _worker(rank, world, port, q):
     try:
+        import time
+
         import oracle
         from paper_2603_15023_b200 import dist as pdist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -65,25 +126,38 @@ def _worker(rank, world, port, q):
         # pac_table_remap; here plain numpy on the oracle's arrays)
         G = len(ukeys)
         idx = np.searchsorted(ukeys, part["keys"])
-        rows = torch.zeros(G, dtype=torch.int64)
-        count = torch.zeros(G, 64, dtype=torch.int64)
+        rows = np.zeros(G, dtype=np.int64)
+        count = np.zeros((G, 64), dtype=np.int64)
+        K = np.zeros(G, dtype=np.uint64)
         worlds = []
-        rows[idx] = torch.from_numpy(part["rows"])
-        count[idx] = torch.from_numpy(part["count"])
+        rows[idx] = part["rows"]
+        count[idx] = part["count"]
+        K[idx] = part["K"]
         for a, k in enumerate(KINDS):
             if k == dg.AGG_COUNT:
                 worlds.append(None)
                 continue
             fill = {dg.AGG_MIN_F64: np.inf, dg.AGG_MAX_F64: -np.inf}.get(k, 0)
-            dt = torch.int64 if k == dg.AGG_SUM_I64 else torch.float64
-            w = torch.full((G, 64), fill, dtype=dt)
-            w[idx] = torch.from_numpy(part["world"][a])
+            w = np.full((G, 64), fill, dtype=np.int64 if k == dg.AGG_SUM_I64 else np.float64)
+            w[idx] = part["world"][a]
             worlds.append(w)
-        pdist.allreduce_table_tensors(rows, count, worlds, KINDS)
-        q.put((rank, ukeys, rows.numpy(), count.numpy(), [None if w is None else w.numpy() for w in worlds]))
+        i64, f64, mn = _pack(G, rows, count, worlds, K)
+        pdist.merge_flat(i64, f64, mn)
+        rows, count, worlds = _unpack(G, i64, f64, mn)
+        # the merge's collectives alone, at BASELINE C5's table size (100 groups, COUNT + SUM + AVG)
+        b = (torch.zeros(100 + 2 * 6400, dtype=torch.int64), torch.zeros(6400, dtype=torch.float64),
+             torch.zeros(3, dtype=torch.int64))
+        for _ in range(5):
+            pdist.merge_flat(*b)
+        t0 = time.perf_counter()
+        for _ in range(50):
+            pdist.merge_flat(*b)
+        us = (time.perf_counter() - t0) / 50 * 1e6
+        q.put((rank, ukeys, rows, count, worlds, us))
         dist.destroy_process_group()
     except Exception as e:  # surface the failure to the parent
-        q.put((rank, "error", repr(e)))
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
 
 
 def test_row_sharded_merge_equals_unsharded_table(orc):
@@ -104,11 +178,11 @@ def test_row_sharded_merge_equals_unsharded_table(orc):
     keep[n // 2:] &= g[n // 2:] != 7   # the rows rank 1 left out
     pu, g, iv, fv = pu[keep], g[keep], iv[keep], fv[keep]
     ref = orc.agg(orc.pac_hash(pu, 99), [g], _aggs(iv, fv))
-    for rank, ukeys, rows, count, worlds in out:
+    for rank, ukeys, rows, count, worlds, us in out:
         np.testing.assert_array_equal(ukeys, ref["keys"])
         np.testing.assert_array_equal(rows, ref["rows"])
         np.testing.assert_array_equal(count, ref["count"])
-        # K re-derived from the merged counts (NCCL has no OR reduction) equals the OR
+        # K from the merged counts (NCCL has no OR reduction) equals the OR
         K = np.array([sum(1 << j for j in range(64) if c[j] > 0) for c in count], dtype=np.uint64)
         np.testing.assert_array_equal(K, ref["K"])
         for a, k in enumerate(KINDS):
@@ -118,6 +192,7 @@ def test_row_sharded_merge_equals_unsharded_table(orc):
                 np.testing.assert_allclose(worlds[a], ref["world"][a], rtol=1e-12)
             else:
                 np.testing.assert_array_equal(worlds[a], ref["world"][a])
+        print(f"rank {rank}: merge collectives at C5 table size {us:.0f} us (gloo, CPU)")
 
 
 def test_reduce_ops_follow_aggregate_kind():

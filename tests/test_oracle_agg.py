@@ -170,3 +170,77 @@ def test_restricting_to_sampled_groups_matches_full_table(orc):
         assert np.array_equal(part["count"][i], full["count"][g])
         assert np.array_equal(part["world"][1][i], full["world"][1][g])
         assert np.array_equal(part["world"][5][i], full["world"][5][g])
+
+
+def _total_order_key(v):
+    # R31 (DuckDB's order on DOUBLE): NaN above every other value, all NaNs equal
+    return (1, 0.0) if np.isnan(v) else (0, v)
+
+
+def _fclass(x):
+    return "nan" if np.isnan(x) else ("+inf" if x == np.inf else ("-inf" if x == -np.inf else "fin"))
+
+
+@pytest.mark.parametrize("method", ["o1", "o2"])
+def test_non_finite_values_follow_ieee_sums_and_total_order_extremes(orc, method):
+    # R30: SUM/AVG of f64 is the IEEE sum (class order-independent: any NaN -> NaN,
+    # +inf with -inf -> NaN, else the infinity); R31: MIN/MAX under the total order with
+    # NaN largest.  Reference: per world, numpy's plain sum for the class and Python's
+    # sorted() with the total-order key for the extremes, on the world's filtered rows.
+    rng = np.random.default_rng(31)
+    n = 400
+    pu = rng.integers(0, 40, n).astype(np.int64)
+    keys = [rng.integers(0, 3, n).astype(np.int32)]
+    fv = rng.normal(0.0, 5.0, n)
+    fv[rng.choice(n, 12, replace=False)] = np.nan
+    fv[rng.choice(n, 8, replace=False)] = np.inf
+    fv[rng.choice(n, 8, replace=False)] = -np.inf
+    # group 3: only NaN rows; group 4: only +inf rows (a present world whose MIN is +inf)
+    keys[0] = np.concatenate([keys[0], [3, 3, 4, 4]]).astype(np.int32)
+    fv = np.concatenate([fv, [np.nan, np.nan, np.inf, np.inf]])
+    pu = np.concatenate([pu, [100, 101, 102, 103]]).astype(np.int64)
+    iv = np.zeros(len(fv), dtype=np.int64)
+    masks = orc.pac_hash(pu, 99)
+    t = orc.agg(masks, keys, [(AGG_COUNT, None), (AGG_SUM_F64, fv), (AGG_MIN_F64, fv), (AGG_MAX_F64, fv)],
+                method=method)
+    B = _bits(masks)
+    for g in range(t["G"]):
+        gk = _unpack_group_key(t["keys"][g], [4])[0]
+        for j in range(64):
+            sel = (keys[0] == gk) & B[:, j]
+            vals = fv[sel]
+            assert t["count"][g, j] == sel.sum()
+            if sel.sum() == 0:
+                assert t["world"][2][g, j] == np.inf and t["world"][3][g, j] == -np.inf
+                continue
+            ref_sum = float(np.sum(vals))
+            got = t["world"][1][g, j]
+            assert _fclass(got) == _fclass(ref_sum)
+            if _fclass(ref_sum) == "fin":
+                np.testing.assert_allclose(got, ref_sum, rtol=1e-12, atol=1e-9)
+            srt = sorted(vals.tolist(), key=_total_order_key)
+            for got_e, ref_e in ((t["world"][2][g, j], srt[0]), (t["world"][3][g, j], srt[-1])):
+                assert _fclass(got_e) == _fclass(ref_e)
+                if _fclass(ref_e) != "nan":
+                    assert got_e == ref_e
+    # the special groups, spelled out
+    g3 = [g for g in range(t["G"]) if _unpack_group_key(t["keys"][g], [4])[0] == 3][0]
+    present = t["count"][g3] > 0
+    assert present.any() and np.all(np.isnan(t["world"][2][g3][present]))
+    assert np.all(np.isnan(t["world"][3][g3][present]))
+    g4 = [g for g in range(t["G"]) if _unpack_group_key(t["keys"][g], [4])[0] == 4][0]
+    present = t["count"][g4] > 0
+    assert np.all(t["world"][2][g4][present] == np.inf) and np.all(t["world"][1][g4][present] == np.inf)
+
+
+def test_non_finite_sum_classes_are_exact(orc):
+    # R30 closed forms on all-ones masks (every world = all rows)
+    ones = np.full(3, 0xFFFFFFFFFFFFFFFF, dtype=np.uint64)
+    for vals, cls in (([1.0, np.inf, 2.0], "+inf"), ([1.0, -np.inf], "-inf"), ([np.inf, -np.inf, 1.0], "nan"),
+                      ([np.nan, 1.0, 2.0], "nan"), ([1e300, -1e300, 3.0], "fin")):
+        v = np.array(vals)
+        t = orc.agg(ones[:len(v)], [], [(AGG_SUM_F64, v), (AGG_MIN_F64, v), (AGG_MAX_F64, v)])
+        assert all(_fclass(x) == cls for x in t["world"][0][0])
+        srt = sorted(vals, key=_total_order_key)
+        assert all(_fclass(x) == _fclass(srt[0]) for x in t["world"][1][0])
+        assert all(_fclass(x) == _fclass(srt[-1]) for x in t["world"][2][0])
