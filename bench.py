@@ -1,19 +1,22 @@
 """bench.py -- PAC grouped-aggregation throughput on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl reference]
 
 A step is one pass of the whole hot path over one batch of synthetic rows (§8 a1-a7):
 fused pac_hash + group-slot resolution + 64-world COUNT/SUM/AVG accumulation + combine
-(+ NCCL allreduce of the partial tables when N > 1) + finalize with posterior updates.
-Default workload: BASELINE.json configs[1] (C2: 6e7 rows per GPU, 6 groups), the config
-the metric is quoted on.  Multi-GPU: one process per GPU (torchrun), each rank aggregates
-its own 6e7-row shard of one global dataset (weak scaling), merged by NCCL allreduce.
+(+ the cross-GPU merge -- pac_merge_pack, three NCCL all_reduce, pac_merge_unpack -- when N > 1)
++ finalize with posterior updates (C5: d = 20 rounds).
+Default workload: BASELINE.json configs[4] (C5: 1.2e9 rows, 100 groups, COUNT + SUM + AVG, 20
+finalize rounds), the configuration the metric is quoted on ("at 1/2/4/8 GPUs").  Multi-GPU: one
+process per GPU (torchrun); the 1.2e9 rows of one global dataset are row-sharded across the ranks
+(strong scaling: rank r owns rows [r n / N, (r + 1) n / N)).
 
-Prints ONE JSON line (rank 0).  `value` = rows/s over all ranks, device-timed with CUDA
-events (max over ranks); `e2e` = the same metric through the public API with pinned-host
-inputs copied H2D and the releases copied D2H inside the timed region; `roofline` = the
-aggregation kernel's algorithmic input bytes / its event-timed duration vs the measured
-HBM copy peak; `cpu_baseline` = the CPU oracle on a bounded sample (rank 0, N=1 only).
+Prints ONE JSON line (rank 0).  `value` = rows/s over all ranks, device-timed with CUDA events
+(max over ranks); `e2e` = the same metric through the public API with pinned-host inputs copied
+H2D and the releases copied D2H inside the timed region; `roofline` = the aggregation pass's
+algorithmic bytes / its event-timed duration vs the measured HBM copy peak, with the issue-slot
+(ALU) fraction beside it; `cpu_baseline` = the CPU oracle on a bounded sample, on every host core
+and on one (rank 0, N = 1 only).
 """
 from __future__ import annotations
 
@@ -41,15 +44,15 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def _traffic(cfg):
-    """Per-launch DRAM bytes of the aggregation kernel from the committed ncu summary."""
+def _profile_entry(cfg):
+    """Per-launch DRAM bytes and warp-instructions per row of the aggregation pass, from the
+    committed ncu summary (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get(cfg, {}).get("dram_bytes_per_launch")
+            return json.load(f).get(cfg, {})
     except Exception:
-        return None
+        return {}
 
 
 class ClockSampler:
@@ -102,57 +105,80 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------- CPU legs
-def oracle_rows_per_s(w, budget_s: float = 12.0, max_rows: int = 4_000_000):
-    max_rows = min(max_rows, w.n_rows)
-    """The CPU oracle (as it stands) on a bounded sample of the workload: rows/s."""
-    import numpy as np
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
+
+def oracle_run(w, n, threads, seed=0xC0FFEE):
+    """The CPU oracle (as it stands) on the first n rows of the workload: pac_hash + O2 (on
+    `threads` host threads: row ranges, partial tables combined in thread order) timed
+    together; finalize (all rounds, sequential by definition) timed separately."""
     import oracle
     oracle.build()
-    seed = 0xC0FFEE
     jstar, salt, P = oracle.session(seed)
-    # calibrate on a small prefix, then size the sample for ~budget_s of CPU work
-    n0 = min(100_000, max_rows)
-    cols = w.host_columns(0, n0)
-    aggs = [(k, None if i < 0 else cols["values"][i]) for k, i in w.aggs]
-    t = time.perf_counter()
-    tab = oracle.agg(oracle.pac_hash(cols["pu"], salt), cols["keys"], aggs)
-    oracle.finalize(seed, w.budget, jstar, P, tab)
-    rate = n0 / (time.perf_counter() - t)
-    n = int(min(max_rows, max(n0, rate * budget_s)))
     cols = w.host_columns(0, n)
     aggs = [(k, None if i < 0 else cols["values"][i]) for k, i in w.aggs]
     t = time.perf_counter()
-    tab = oracle.agg(oracle.pac_hash(cols["pu"], salt), cols["keys"], aggs)
-    oracle.finalize(seed, w.budget, jstar, P, tab)
-    el = time.perf_counter() - t
-    return n / el, n, el
+    if threads > 1:
+        tab = oracle.agg_mt(oracle.pac_hash_mt(cols["pu"], salt, threads), cols["keys"], aggs, threads)
+    else:
+        tab = oracle.agg(oracle.pac_hash(cols["pu"], salt), cols["keys"], aggs)
+    t_agg = time.perf_counter() - t
+    t = time.perf_counter()
+    for r in range(w.rounds):
+        _, _, _, _, P = oracle.finalize(seed, w.budget, jstar, P, tab, r)
+    t_fin = time.perf_counter() - t
+    return t_agg, t_fin
+
+
+def cpu_baseline(w, budget_s=20.0, max_rows=100_000_000):
+    """Rows/s of the oracle on all host cores (bounded sample of ~budget_s of CPU work, calibrated
+    on a prefix) and on one core; aggregation and finalize timed separately."""
+    cores = os.cpu_count() or 1
+    n0 = min(200_000, w.n_rows)
+    a0, f0 = oracle_run(w, n0, 1)
+    rate1 = n0 / a0
+    n = int(min(w.n_rows, max(n0, rate1 * cores * budget_s * 0.5)))
+    if max_rows:
+        n = min(n, max_rows)
+    a_all, f_all = oracle_run(w, n, cores)
+    n1 = int(min(n, max(n0, rate1 * budget_s * 0.25)))
+    a_one, _ = oracle_run(w, n1, 1)
+    return {
+        "value": n / (a_all + f_all), "unit": "rows/s", "cores": cores, "kind": "oracle",
+        "cpu_model": _cpu_model(),
+        "sample": f"first {n} rows of {w.name}: oracle pac_hash + O2 on {cores} threads "
+                  f"({a_all:.2f} s) + finalize x{w.rounds} rounds ({f_all:.3f} s)",
+        "agg_rows_per_s": n / a_all, "finalize_s": f_all,
+        "one_core": {"rows": n1, "agg_rows_per_s": n1 / a_one},
+    }
 
 
 def run_reference(args, w):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import numpy as np  # noqa: F401
     steps_val = []
-    sample = None
+    per = max(2.0, args.ref_seconds / max(1, args.warmup + args.steps))
+    cb = None
     for i in range(args.warmup + args.steps):
-        v, n, el = oracle_rows_per_s(w, budget_s=max(min(2.0, args.ref_seconds),
-                                                     args.ref_seconds / max(1, args.warmup + args.steps)),
-                                     max_rows=2_000_000)
+        cb = cpu_baseline(w, budget_s=per)
         if i >= args.warmup:
-            steps_val.append(v)
-        sample = n
+            steps_val.append(cb["value"])
     val = statistics.median(steps_val)
-    cores = 1
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "rows/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sample / val * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i64+f64",
-        "data": "synthetic", "config": {"workload": w.name, "rows_per_step": sample,
-                                        "description": w.description},
-        "cpu_baseline": {"value": val, "unit": "rows/s", "cores": cores, "kind": "oracle",
-                         "sample": f"first {sample} rows of {w.name} per step (oracle O2 + finalize, 1 thread)"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * w.n_rows / val,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i64+f64",
+        "data": "synthetic", "config": {"workload": w.name, "rows": w.n_rows, "description": w.description},
+        "cpu_baseline": dict(cb, value=val),
         "e2e": {"value": val, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -165,13 +191,14 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--rows", type=int, default=0, help="override rows per GPU (testing only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=60.0,
                     help="--impl reference: total CPU seconds the oracle samples take")
+    ap.add_argument("--weak", action="store_true", help="every rank aggregates the full config (weak scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -200,8 +227,11 @@ def main():
         if world > 1:
             tdist.barrier()
 
-    n = w.n_rows
-    row0 = rank * n  # weak scaling: rank r owns rows [r*n, (r+1)*n) of one global dataset
+    if args.weak:
+        n, row0 = w.n_rows, rank * w.n_rows  # weak: rank r owns rows [r n, (r + 1) n) of one dataset
+    else:  # strong: the config's rows are row-sharded across the ranks
+        row0 = w.n_rows * rank // world
+        n = w.n_rows * (rank + 1) // world - row0
     cols = dg.device_columns(w, row0, n, device=dev)
     keys = cols["keys"]
     vals = [None if i < 0 else cols["values"][i] for _, i in w.aggs]
@@ -217,8 +247,8 @@ def main():
 
     def step(pu, keys_, vals_):
         t = ag(vals_, keys_, pu_key=pu, salt=sess.salt)
-        if world > 1:
-            t = pdist.merge_table(t, list(zip(kinds, vals_)))
+        if world > 1:  # dense domains: every shard holds every group (checked on the device)
+            t = pdist.merge_table(t, list(zip(kinds, vals_)), same_keys=w.name != "C3")
         for r in range(w.rounds):
             fin(sess, t, r)
         return t
@@ -252,7 +282,11 @@ def main():
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         ms, k_ms = float(t[0]), float(t[1])
     ms_step = ms / args.steps
-    value = (n * world) / (ms_step / 1e3)
+    total_rows = n * world if args.weak else w.n_rows
+    value = total_rows / (ms_step / 1e3)
+    status = int(ag.table.status.item())  # after the timed region: a merge or capacity error is fatal
+    if status != 0:
+        raise RuntimeError(f"table status {status} after the timed steps")
 
     # ---- end-to-end through the public API: pinned host inputs H2D + releases D2H
     host = {"pu": cols["pu"].cpu().pin_memory(), "keys": [k.cpu().pin_memory() for k in keys]}
@@ -295,38 +329,50 @@ def main():
         t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         e_ms = float(t[0])
-    e2e_value = (n * world) / (e_ms / args.e2e_steps / 1e3)
+    e2e_value = total_rows / (e_ms / args.e2e_steps / 1e3)
 
     if rank == 0:
         peak, peak_src = _peaks()
-        alg_bytes = n * w.in_bytes_per_row
+        prof = _profile_entry(w.name)
+        # algorithmic bytes of one aggregation pass on this rank: the input columns,
+        # plus the [G][64] table arrays written once (only material for C3's ~1e6 groups)
+        arrays = 1 + sum(1 for k in kinds if k != pac.COUNT)
+        alg_bytes = n * w.in_bytes_per_row + (G * 64 * 8 * arrays if w.name == "C3" else 0)
         k_avg_ms = k_ms / max(1, k_n)
         achieved = alg_bytes / (k_avg_ms / 1e3) / 1e9
+        clocks = clk.summary()
+        f_sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
+        issue_peak = 148 * 4 * f_sm  # warp-instructions/s: 148 SMs x 4 schedulers x 1 issue/clk
+        wipr = prof.get("warp_instr_per_row")
+        traffic = prof.get("dram_bytes_per_row")
         line = {
             "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None, "dtype": "i64+f64", "data": "synthetic",
-            "config": {"workload": w.name, "rows_per_gpu": n, "groups": G, "aggregates": len(kinds),
-                       "finalize_rounds": w.rounds, "in_bytes_per_row": w.in_bytes_per_row,
-                       "l2": f"inputs {alg_bytes / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)",
+            "config": {"workload": w.name, "rows": total_rows, "rows_per_gpu": n, "groups": G,
+                       "aggregates": len(kinds), "finalize_rounds": w.rounds,
+                       "in_bytes_per_row": w.in_bytes_per_row,
+                       "l2": f"inputs {n * w.in_bytes_per_row / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)",
                        "description": w.description},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": _traffic(w.name),
-                         "kernel": "k_agg_tiles (pac_agg_grouped main kernel)",
+                         "frac": achieved / peak,
+                         "traffic": None if traffic is None else traffic * n,
+                         "kernel": pac.profile_last_kernel(),
                          "kernel_ms": k_avg_ms, "kernel_share_of_step": k_avg_ms / ms_step,
-                         "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": alg_bytes},
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
+                         "profile_source": prof.get("source"),
+                         "alu_issue": None if wipr is None else {
+                             "warp_instr_per_row": wipr, "peak_warp_instr_per_s": issue_peak,
+                             "frac": wipr * n / (k_avg_ms / 1e3) / issue_peak}},
             "e2e": {"value": e2e_value, "unit": "rows/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         if world == 1 and not args.no_cpu_baseline:
             try:
-                v, ns, el = oracle_rows_per_s(w)
-                line["cpu_baseline"] = {"value": v, "unit": "rows/s", "cores": 1, "kind": "oracle",
-                                        "sample": f"first {ns} rows of {w.name} (oracle pac_hash + O2 + "
-                                                  f"finalize, 1 thread, {el:.1f} s)"}
+                line["cpu_baseline"] = cpu_baseline(w)
             except Exception as e:  # report, never hide
                 line["cpu_baseline"] = {"value": None, "error": repr(e)}
         print(json.dumps(line), flush=True)

@@ -35,6 +35,18 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _includes(src, seen=None):
+    """src plus every local header it includes, recursively (#include "...")."""
+    import re
+    seen = set() if seen is None else seen
+    if src in seen or not os.path.exists(src):
+        return seen
+    seen.add(src)
+    for inc in re.findall(r'^\s*#\s*include\s+"([^"]+)"', open(src).read(), flags=re.M):
+        _includes(os.path.normpath(os.path.join(os.path.dirname(src), inc)), seen)
+    return seen
+
+
 def build_cuda(name: str, force: bool = False, verbose: bool = False) -> str:
     """Compile every .cu of the target to an object in parallel, then link the .so."""
     out, srcs, hdrs = TARGETS[name]
@@ -45,6 +57,8 @@ def build_cuda(name: str, force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        if not force and os.path.exists(obj) and not _stale(obj, _includes(src)):
+            return src, obj, None  # object newer than the source and every header it includes
         cmd = [NVCC] + ARCH + NVFLAGS + ["-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]
         r = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, r
@@ -53,6 +67,8 @@ def build_cuda(name: str, force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(os.cpu_count() or 8, len(srcs))) as ex:
         results = list(ex.map(compile_one, srcs))
     for src, obj, r in results:
+        if r is None:
+            continue
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed for {src}")

@@ -20,6 +20,7 @@
 
 #include "agg_tiles.cuh"
 #include "agg_tm.cuh"
+#include "agg_ws.cuh"
 
 namespace pac {
 
@@ -1006,6 +1007,26 @@ static const LaunchFn kLaunchTm[3][3][4] = {
     {PAC_TMM_ROW(2, 0), PAC_TMM_ROW(2, 1), PAC_TMM_ROW(2, 2)},
 };
 
+typedef cudaError_t (*WsFn)(const AggPlan&, const WskLayout&, int, cudaStream_t);
+extern template cudaError_t launch_ws<0, 0, 0>(const AggPlan&, const WskLayout&, int, cudaStream_t);
+extern template cudaError_t launch_ws<0, 1, 0>(const AggPlan&, const WskLayout&, int, cudaStream_t);
+extern template cudaError_t launch_ws<0, 2, 0>(const AggPlan&, const WskLayout&, int, cudaStream_t);
+extern template cudaError_t launch_ws<1, 0, 0>(const AggPlan&, const WskLayout&, int, cudaStream_t);
+extern template cudaError_t launch_ws<1, 1, 0>(const AggPlan&, const WskLayout&, int, cudaStream_t);
+extern template cudaError_t launch_ws<1, 2, 0>(const AggPlan&, const WskLayout&, int, cudaStream_t);
+extern template cudaError_t launch_ws<2, 0, 0>(const AggPlan&, const WskLayout&, int, cudaStream_t);
+extern template cudaError_t launch_ws<2, 1, 0>(const AggPlan&, const WskLayout&, int, cudaStream_t);
+extern template cudaError_t launch_ws<2, 2, 0>(const AggPlan&, const WskLayout&, int, cudaStream_t);
+static const WsFn kLaunchWs[3][3] = {
+    {launch_ws<0, 0, 0>, launch_ws<0, 1, 0>, launch_ws<0, 2, 0>},
+    {launch_ws<1, 0, 0>, launch_ws<1, 1, 0>, launch_ws<1, 2, 0>},
+    {launch_ws<2, 0, 0>, launch_ws<2, 1, 0>, launch_ws<2, 2, 0>},
+};
+static bool ws_tmem_ok(const AccSet& A, const WskLayout& L) {
+  const int wps = 2 + 4 * A.ni + 4 * A.nf + (A.has_min ? 4 : 0) + (A.has_max ? 4 : 0);
+  return ws_tmem_fits(L, wps);
+}
+
 typedef void (*SpillFn)(const AggPlan&, const unsigned long long*, const int2*, int, cudaStream_t);
 template <int NI, int NF, int MM>
 static void launch_spill(const AggPlan& p, const unsigned long long* tot, const int2* pairs, int grid,
@@ -1174,6 +1195,31 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
       k_agg_minmax<<<grid, kThreads, L.bytes, st>>>(p, L);
       note_launch();
       e = cudaGetLastError();
+      profile_end(st);
+    } else if (A.has_min == 0 && A.has_max == 0 && G_cap <= 128 && getenv("PAC_WS") &&
+               ws_tmem_ok(A, wsk_layout(A.ni, A.nf, 0, (int)G_cap)) &&
+               wsk_layout(A.ni, A.nf, 0, (int)G_cap).bytes <= smem_max && wsk_layout(A.ni, A.nf, 0, (int)G_cap).mine <= 32) {
+      // every group fits a local slot: the warp-specialized kernel (agg_ws.cuh; opt-in with PAC_WS=1 --
+      // measured slower than the tile kernels on C2 / C5)
+      const WskLayout WL = wsk_layout(A.ni, A.nf, 0, (int)G_cap);
+      bool aligned = true;
+      p.nraw = 0;
+      auto add = [&](const void* col, int eb) {
+        p.raw_src[p.nraw] = col;
+        p.raw_eb[p.nraw] = eb;
+        p.raw_off[p.nraw] = 0;
+        aligned = aligned && (((uintptr_t)col) & 15) == 0;
+        ++p.nraw;
+      };
+      add(d_mask ? (const void*)d_mask : (const void*)d_pu_key, 8);
+      for (int c = 0; c < A.ni; ++c) add(A.icol[c], 8);
+      for (int c = 0; c < A.nf; ++c) add(A.fcol[c], 8);
+      for (int c = 0; c < n_keys; ++c) add(keys[c].d_col, keys[c].elem_bytes);
+      p.tma_ok = aligned ? 1 : 0;  // 16-byte aligned columns: bulk L2 prefetch of upcoming chunks
+      char kname[64];
+      snprintf(kname, sizeof(kname), "k_agg_ws<%d,%d,0>", A.ni, A.nf);
+      profile_begin(st, kname);
+      e = kLaunchWs[A.ni][A.nf](p, WL, sms, st);
       profile_end(st);
     } else {
       SmemLayout L{};
