@@ -210,11 +210,20 @@ static __device__ int global_slot(const AggPlan& p, uint64_t key) {
 // inserted (their rows use the HBM dictionary directly).
 // defer: a key the full dictionary cannot take returns kUnresolved instead of its HBM slot (the
 // deferred tier resolves it after the pass, k_spill_resolve).
+// acquire load of a shared-memory word (an LDS: CTA-scope acquire on shared memory needs no fence)
+__device__ __forceinline__ int ld_acquire_cta_shared(const int* a) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(a))
+               : "memory");
+  return v;
+}
+
 static __device__ int local_code(const AggPlan& p, uint64_t key, unsigned long long* lkey, int* lstate,
                           int LH, int* lprov, int Lcap, Misc* misc, bool defer = false) {
   uint32_t h = (((uint32_t)key ^ (uint32_t)(key >> 32)) * 0x9E3779B1u) >> 16 & (LH - 1);
   for (;;) {
-    int st = *(volatile int*)&lstate[h];
+    // acquire: a published state (the writer fences before publishing) orders the key read after it
+    const int st = ld_acquire_cta_shared(&lstate[h]);
     if (st == 0) {
       // a full dictionary stays full: skip the claim-and-release
       if (*(volatile int*)&misc->ndict >= LH / 2) return defer ? kUnresolved : kOvfBase + global_slot(p, key) + 1;
@@ -242,7 +251,6 @@ static __device__ int local_code(const AggPlan& p, uint64_t key, unsigned long l
       continue;
     }
     if (st < 0) continue;
-    __threadfence_block();
     if (*(volatile unsigned long long*)&lkey[h] == key) return st;
     h = (h + 1) & (LH - 1);
   }

@@ -161,7 +161,7 @@ __device__ __forceinline__ bool ws_try_write(const WsSmem& sm, const WskLayout& 
 #pragma unroll
   for (int c = 0; c < NV; ++c) b[32 * (1 + c) + i] = v[c];
   if (f) atomicOr(&sm.flag[pair], f);
-  __threadfence_block();
+  asm volatile("fence.acq_rel.cta;" ::: "memory");
   if (atomicAdd(&sm.cnt[pair], 1) == 31) {  // the run is full: tell its owner
     int idx;
     const int owner = ws_owner(L, pair, idx);
@@ -233,7 +233,7 @@ template <int NI, int NF, int MM>
 __device__ __forceinline__ void ws_consume(const WsSmem& sm, const WskLayout& L, int pair, int len, uint32_t taddr,
                                            const XposeConst& xc, int lane) {
   constexpr int NV = NI + NF + (MM ? 1 : 0);
-  __threadfence_block();  // acquire: the count was read; now the rows
+  asm volatile("fence.acq_rel.cta;" ::: "memory");  // acquire: the count was read; now the rows
   const unsigned long long* b = (const unsigned long long*)(sm.buf + (size_t)pair * (32 * 8 * (1 + NV)));
   const int f = ld_vol(&sm.flag[pair]);
   WarpAcc<NI, NF, MM> acc;
@@ -251,7 +251,7 @@ __device__ __forceinline__ void ws_consume(const WsSmem& sm, const WskLayout& L,
   if (lane == 0) {
     sm.flag[pair] = 0;
     sm.cnt[pair] = 0;
-    __threadfence_block();
+    asm volatile("fence.acq_rel.cta;" ::: "memory");
     atomicAdd(&sm.gen[pair], 1);  // release: the next run may be written
   }
   __syncwarp();
@@ -297,7 +297,7 @@ __device__ void ws_service(const WsSmem& sm, const WskLayout& L, uint32_t tmine,
     __syncwarp();
     pn = __popc(km);
     if (lane == 0 && okm) {
-      __threadfence_block();
+      asm volatile("fence.acq_rel.cta;" ::: "memory");
       atomicSub(&sm.misc->pending, __popc(okm));
     }
   }
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_agg_ws(AggPlan p, WskLayout L
   }
   __syncwarp();
   if (lane == 0) {
-    __threadfence_block();
+    asm volatile("fence.acq_rel.cta;" ::: "memory");
     atomicAdd(&sm.misc->done, 1);
   }
   // keep servicing until every warp is done and no write is pending anywhere: after that no row
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_agg_ws(AggPlan p, WskLayout L
     __nanosleep(nap);
     nap = nap < 1024 ? 2 * nap : 1024;
   }
-  __threadfence_block();
+  asm volatile("fence.acq_rel.cta;" ::: "memory");
   ws_service<NI, NF, MM>(sm, L, tmine, xc, wid, lane, pn);
   for (int i = 0; i < L.mine; ++i) {
     int k;

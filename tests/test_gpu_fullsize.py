@@ -79,3 +79,95 @@ def test_full_size_sampled_parity(orc, cfg):
                 ref = torch.full((G,), empty, dtype=torch.float64).scatter_reduce_(
                     0, inv_t[sel_t], torch.from_numpy(v)[sel_t], reduce=red, include_self=True)
                 np.testing.assert_array_equal(got["world"][a][:, j], ref.numpy())
+
+
+def _threads():
+    import os
+    return max(1, os.cpu_count() or 1)
+
+
+def test_c2_full_table_all_worlds_and_releases(orc):
+    """C2 at 6e7 rows (bench launch configuration): the complete 64-world table against O2 (row
+    ranges on every host core, partial tables combined in thread order -- f64 sums within R16),
+    then one finalize round: releases, NULL flags, diversity flags and the posterior."""
+    from gpu_helpers import assert_delta_close, assert_releases_close, assert_tables_equal
+    w = dg.WORKLOADS["C2"]
+    cols = w.host_columns(0, w.n_rows)
+    aggs = [(k, None if i < 0 else cols["values"][i]) for k, i in w.aggs]
+    seed = 0x5EED
+    s = pac.Session(seed, w.budget)
+    ag = pac.Aggregator([k for k, _ in aggs], BENCH_G_CAP["C2"])
+    t = ag([None if v is None else to_dev(v) for _, v in aggs], [to_dev(k) for k in cols["keys"]],
+           pu_key=to_dev(cols["pu"]), salt=s.salt)
+    got = t.to_host()
+    n = _threads()
+    ref = orc.agg_mt(orc.pac_hash_mt(cols["pu"], s.salt, n), cols["keys"], aggs, n)
+    assert_tables_equal(got, ref)
+    jstar, salt, P = orc.session(seed)
+    rel, isn, flags, delta = pac.finalize(s, t, 0)
+    r_o, n_o, f_o, d_o, P = orc.finalize(seed, w.budget, jstar, P, ref, 0)
+    G = ref["G"]
+    assert_releases_close(rel[:G].cpu().numpy(), r_o, d_o, isn[:G].cpu().numpy(), n_o)
+    np.testing.assert_array_equal(flags[:G].cpu().numpy(), f_o)
+    ok = n_o == 0
+    ymax = np.abs(r_o[ok]).max() if ok.any() else 1.0
+    assert_delta_close(delta[:G].cpu().numpy()[ok], d_o[ok], ymax, w.budget)
+    np.testing.assert_allclose(s.query()["P"], P, rtol=0, atol=1e-9)
+
+
+def test_c5_full_size_sampled_groups_and_twenty_rounds(orc):
+    """C5 at 1.2e9 rows in bench.py's launch configuration (G_cap = 100; device-generated columns,
+    as bench.py times them).  Every group: rows and sum_j COUNT_j = 32 rows.  Two sampled groups:
+    the rows of those groups are selected on the device, copied to the host, and the oracle
+    (pac_hash + O2 on every host core) recomputes their complete 64-world tables.  Then all 20
+    finalize rounds of a session over the sampled groups' table (GPU kernels on the GPU table,
+    orc_finalize on the oracle's)."""
+    from gpu_helpers import assert_releases_close, assert_tables_equal
+    w = dg.WORKLOADS["C5"]
+    cols = dg.device_columns(w, 0, w.n_rows)
+    kinds = [k for k, _ in w.aggs]
+    vals = [None if i < 0 else cols["values"][i] for _, i in w.aggs]
+    seed = 0x5EED
+    s = pac.Session(seed, w.budget)
+    ag = pac.Aggregator(kinds, 100)
+    t = ag(vals, cols["keys"], pu_key=cols["pu"], salt=s.salt)
+    got = t.to_host()
+    g = cols["keys"][0]
+    rows = torch.bincount(g.long(), minlength=100).cpu().numpy()
+    assert got["G"] == 100
+    np.testing.assert_array_equal(got["rows"], rows)
+    np.testing.assert_array_equal(got["count"].sum(axis=1), 32 * rows)
+    pick = [7, 64]
+    sel = (g == pick[0]) | (g == pick[1])
+    sub_pu = cols["pu"][sel].cpu().numpy()
+    sub_g = g[sel].cpu().numpy()
+    sub_v = {i: v[sel].cpu().numpy() for i, v in enumerate(cols["values"])}
+    del cols, vals, sel
+    aggs = [(k, None if i < 0 else sub_v[i]) for k, i in w.aggs]
+    n = _threads()
+    ref = orc.agg_mt(orc.pac_hash_mt(sub_pu, s.salt, n), [sub_g], aggs, n)
+    assert ref["G"] == 2
+    gi = [int(np.searchsorted(got["keys"], k)) for k in ref["keys"]]
+    sub = {"G": 2, "keys": got["keys"][gi], "rows": got["rows"][gi], "K": got["K"][gi], "count": got["count"][gi],
+           "world": [None if x is None else x[gi] for x in got["world"]], "kinds": got["kinds"]}
+    assert_tables_equal(sub, ref)
+    # the sampled groups as a table of their own on the device: 20 finalize rounds
+    t2 = pac.PacTable.allocate(kinds, 2, t.rows.device)
+    idx = torch.tensor(gi, device=t.rows.device)
+    t2.num_groups.fill_(2)
+    t2.status.zero_()
+    t2.group_key.copy_(t.group_key[idx])
+    t2.rows.copy_(t.rows[idx])
+    t2.presence.copy_(t.presence[idx])
+    t2.count.copy_(t.count[idx])
+    for a, x in enumerate(t.world):
+        if x is not None:
+            t2.world[a].copy_(x[idx])
+    s2 = pac.Session(seed + 1, w.budget)
+    jstar, _, P = orc.session(seed + 1)
+    fin = pac.Finalizer(kinds, 2)
+    for r in range(w.rounds):
+        rel, isn, _, _ = fin(s2, t2, r)
+        r_o, n_o, _, d_o, P = orc.finalize(seed + 1, w.budget, jstar, P, ref, r)
+        assert_releases_close(rel.cpu().numpy(), r_o, d_o, isn.cpu().numpy(), n_o)
+    np.testing.assert_allclose(s2.query()["P"], P, rtol=0, atol=1e-9)
