@@ -33,11 +33,39 @@ __global__ void __launch_bounds__(256) k_mask(const long long* __restrict__ key,
 }
 
 // ------------------------------------------------------------------ k_agg_minmax (pruned)
+constexpr int kMMQueue = 64;  // k_agg_minmax_v: candidate rows queued per warp
+#ifndef PAC_MM_HINT_EVERY
+#define PAC_MM_HINT_EVERY 8
+#endif
+constexpr int kMMHintEvery = PAC_MM_HINT_EVERY;  // tiles between pulls of the per-slot bound hints
 struct MMLayout {
   int Lcap, LH;
-  int o_lkey, o_lstate, o_lprov, o_lrows, o_bmin, o_bmax, o_dirty, o_misc;
+  int o_lkey, o_lstate, o_lprov, o_lrows, o_bmin, o_bmax, o_dirty, o_misc, o_qr, o_qv, o_qp;
   int bytes;
 };
+
+#ifndef PAC_MM_LH
+#define PAC_MM_LH 4
+#endif
+__host__ __device__ constexpr MMLayout mm_layout_for(int Lcap) {
+  MMLayout L{};
+  L.Lcap = Lcap;
+  L.LH = lay_pow2(PAC_MM_LH * Lcap > 256 ? PAC_MM_LH * Lcap : 256);
+  int off = 0;
+  L.o_lkey = lay_take(off, L.LH * 8);
+  L.o_lrows = lay_take(off, Lcap * 4);
+  L.o_bmin = lay_take(off, Lcap * 8);
+  L.o_bmax = lay_take(off, Lcap * 8);
+  L.o_lstate = lay_take(off, L.LH * 4);
+  L.o_lprov = lay_take(off, Lcap * 4);
+  L.o_dirty = lay_take(off, (kThreads / 32) * ((Lcap + 31) / 32) * 4);  // per-warp dirty bitmaps
+  L.o_misc = lay_take(off, (int)sizeof(Misc));
+  L.o_qr = lay_take(off, (kThreads / 32) * kMMQueue * 8);  // candidate queue: row, value, (prov, slot)
+  L.o_qv = lay_take(off, (kThreads / 32) * kMMQueue * 8);
+  L.o_qp = lay_take(off, (kThreads / 32) * kMMQueue * 8);
+  L.bytes = off;
+  return L;
+}
 
 // Rows per thread per tile: their loads are all issued before any is used, so a thread keeps
 // kMMRows independent row loads in flight (the pruned path is memory-latency bound otherwise).
@@ -206,6 +234,287 @@ __global__ void __launch_bounds__(kThreads, PAC_MM_MINB) k_agg_minmax(AggPlan p,
       }
       if (bits) wdirty[wb + lane] = 0u;
     }
+    __syncwarp();
+  }
+  __syncthreads();
+  const int nloc = min(misc->nlocal, Lcap);
+  for (int s = tid; s < nloc; s += nth)
+    if (lprov[s] >= 0 && lrows[s]) atomicAdd(&p.prov_rows[lprov[s]], (unsigned long long)lrows[s]);
+}
+
+// refresh of the double-valued bounds of k_agg_minmax_v: min_j MAX_j and max_j MIN_j decoded, NaN
+// when some world is still empty (or the bound is NaN) -- a NaN bound admits every row
+__device__ __forceinline__ void mmv_refresh(const AggPlan& p, int pv, int s, double* bmin, double* bmax, int lane) {
+  const size_t b = (size_t)pv * kM;
+  if (p.has_max) {
+    long long a = min(*(volatile long long*)&p.prov_max[b + lane], *(volatile long long*)&p.prov_max[b + lane + 32]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, d));
+    if (lane == 0) {
+      bmax[s] = a == kMaxEmpty ? __longlong_as_double(kEncNaN) : dec_f64(a);
+      if (a != kMaxEmpty) atomicMax(&p.gbmax[pv], a);  // the bound only grows: keep the latest
+    }
+  }
+  if (p.has_min) {
+    long long a = max(*(volatile long long*)&p.prov_min[b + lane], *(volatile long long*)&p.prov_min[b + lane + 32]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) a = max(a, __shfl_xor_sync(0xffffffffu, a, d));
+    if (lane == 0) {
+      bmin[s] = a == kMinEmpty ? __longlong_as_double(kEncNaN) : dec_f64(a);
+      if (a != kMinEmpty) atomicMin(&p.gbmin[pv], a);
+    }
+  }
+}
+
+// CTA dictionary for one int32 key column: entry = (code << 32) | packed key in one 64-bit word
+// (0 = empty; code 0xFFFFFFFF = being written), so a lookup is one shared load and one compare.
+// Codes as local_code's: s + 1 for local slot s, kOvfBase + HBM slot + 1 for a key with none.
+__device__ __forceinline__ unsigned long long ld_acquire_cta_shared_u64(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"((uint32_t)__cvta_generic_to_shared(a))
+               : "memory");
+  return v;
+}
+static __device__ int local_code32(const AggPlan& p, uint32_t key, unsigned long long* dent, int LH, int* lprov,
+                                   int Lcap, Misc* misc, double* bmin, double* bmax) {
+  uint32_t h = (key * 0x9E3779B1u) >> 16 & (LH - 1);
+  for (;;) {
+    const unsigned long long e = ld_acquire_cta_shared_u64(&dent[h]);
+    if (e != 0ull && (uint32_t)e == key) {
+      const uint32_t code = (uint32_t)(e >> 32);
+      if (code == 0xFFFFFFFFu) continue;  // being written
+      return (int)code;
+    }
+    if (e == 0ull) {
+      if (*(volatile int*)&misc->ndict >= LH / 2) return kOvfBase + global_slot(p, (uint64_t)key) + 1;
+      if (atomicCAS(&dent[h], 0ull, 0xFFFFFFFF00000000ull | key) == 0ull) {
+        if (atomicAdd(&misc->ndict, 1) >= LH / 2) {  // too full: release, use the HBM tier
+          atomicSub(&misc->ndict, 1);
+          __threadfence_block();
+          atomicExch(&dent[h], 0ull);
+          return kOvfBase + global_slot(p, (uint64_t)key) + 1;
+        }
+        const int sl = atomicAdd(&misc->nlocal, 1);
+        const int prov = global_slot(p, (uint64_t)key);
+        int code;
+        if (sl < Lcap) {
+          lprov[sl] = prov;
+          code = sl + 1;
+          // a slot new to this CTA starts from the group's published bounds (other CTAs' progress)
+          if (prov >= 0 && p.gbmax) {
+            const long long g = __ldcg(p.gbmax + prov);
+            if (g != kMaxEmpty) bmax[sl] = dec_f64(g);
+          }
+          if (prov >= 0 && p.gbmin) {
+            const long long g = __ldcg(p.gbmin + prov);
+            if (g != kMinEmpty) bmin[sl] = dec_f64(g);
+          }
+        } else {
+          code = kOvfBase + prov + 1;
+        }
+        __threadfence_block();
+        atomicExch(&dent[h], ((unsigned long long)(uint32_t)code << 32) | key);
+        return code;
+      }
+      continue;
+    }
+    h = (h + 1) & (LH - 1);
+  }
+}
+
+// The pruned MIN/MAX kernel for the common layout (one int32 group-key column, pu keys hashed in
+// the kernel, 16-byte aligned columns -- BASELINE C4).  Each thread takes ROWS consecutive rows
+// per tile with 16-byte loads; MIN / MAX are compile-time; the bounds are cached as doubles (NaN =
+// admit every row: some world still empty) so the pruning test is one FP64 compare that is also
+// true for a NaN value (!(v <= bound)).  Rows that pass it (candidates) are queued per warp and
+// applied 32 at a time -- every lane hashes one candidate's pu key, then the warp applies them one
+// by one (lane j: worlds j, j + 32, atomicMax / atomicMin on the order-preserving encodings, R31)
+// -- instead of the whole warp hashing whenever one lane has a candidate.  Bounds: after applying,
+// the warp refreshes the slots it updated from the HBM table and publishes the result as a per-slot
+// hint (gbmin / gbmax, monotone); at every tile each CTA pulls the hints of all its slots, so its
+// bounds follow the other CTAs' progress and stale bounds admit few rows.
+template <int MM>
+__device__ __forceinline__ void mmv_apply(const AggPlan& p, const int64_t* qr, const double* qv, const int2* qp,
+                                          int qh, int n, unsigned* wdirty, double* bmin, double* bmax,
+                                          const int* lprov, int lane) {
+  uint64_t m = 0;
+  long long e = 0;
+  int pv = -1, sl = -1;
+  if (lane == 0) atomicAdd(&p.dbg[0], (unsigned long long)n);  // candidates (PAC_DEBUG statistic)
+  if (lane < n) {
+    const int i = (qh + lane) & (kMMQueue - 1);
+    m = pac_hash_dev((uint64_t)__ldg(p.pu_key + qr[i]), p.salt);
+    e = enc_f64(qv[i]);
+    pv = qp[i].x;
+    sl = qp[i].y;
+  }
+  for (int src = 0; src < n; ++src) {
+    const uint64_t mm = __shfl_sync(0xffffffffu, m, src);
+    const long long es = __shfl_sync(0xffffffffu, e, src);
+    const int pvs = __shfl_sync(0xffffffffu, pv, src);
+    const int ss = __shfl_sync(0xffffffffu, sl, src);
+    const size_t b = (size_t)pvs * kM;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if ((mm >> (lane + 32 * h)) & 1ull) {
+        if (MM & 2) atomicMax(&p.prov_max[b + lane + 32 * h], es);
+        if (MM & 1) atomicMin(&p.prov_min[b + lane + 32 * h], es);
+      }
+    }
+    if (lane == 0 && ss >= 0) wdirty[ss >> 5] |= 1u << (ss & 31);
+  }
+}
+
+template <int MM, int ROWS, int LC>
+__global__ void __launch_bounds__(kThreads, PAC_MM_MINB) k_agg_minmax_v(AggPlan p, MMLayout Lp) {
+  // LC > 0: the layout of LC local slots as a compile-time constant (immediate smem offsets)
+  constexpr MMLayout Lc = mm_layout_for(LC > 0 ? LC : 1);
+  const MMLayout& L = LC > 0 ? Lc : Lp;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long* lkey = (unsigned long long*)(smem + L.o_lkey);
+  int* lstate = (int*)(smem + L.o_lstate);
+  int* lprov = (int*)(smem + L.o_lprov);
+  unsigned* lrows = (unsigned*)(smem + L.o_lrows);
+  double* bmin = (double*)(smem + L.o_bmin);  // max_j MIN_j, cached (NaN: admit every row)
+  double* bmax = (double*)(smem + L.o_bmax);  // min_j MAX_j, cached (NaN: admit every row)
+  Misc* misc = (Misc*)(smem + L.o_misc);
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int Lcap = L.Lcap, LH = L.LH;
+  const int nwords = (Lcap + 31) >> 5;
+  unsigned* wdirty = (unsigned*)(smem + L.o_dirty) + wid * nwords;
+  int64_t* qr = (int64_t*)(smem + L.o_qr) + wid * kMMQueue;
+  double* qv = (double*)(smem + L.o_qv) + wid * kMMQueue;
+  int2* qp = (int2*)(smem + L.o_qp) + wid * kMMQueue;
+
+  for (int i = tid; i < LH; i += nth) lkey[i] = 0ull;  // the packed int32 dictionary (local_code32)
+  for (int i = tid; i < Lcap; i += nth) {
+    lrows[i] = 0;
+    lprov[i] = -1;
+    bmin[i] = __longlong_as_double(kEncNaN);  // nothing can be pruned until every world holds a value
+    bmax[i] = __longlong_as_double(kEncNaN);
+  }
+  for (int i = lane; i < nwords; i += 32) wdirty[i] = 0u;
+  if (tid == 0) {
+    misc->nlocal = 0;
+    misc->ndict = 0;
+  }
+  __syncthreads();
+
+  auto refresh_dirty = [&]() {
+    for (int wb = 0; wb < nwords; wb += 32) {
+      const unsigned bits = wb + lane < nwords ? wdirty[wb + lane] : 0u;
+      unsigned have = __ballot_sync(0xffffffffu, bits != 0u);
+      while (have) {
+        const int src = __ffs(have) - 1;
+        have &= have - 1;
+        unsigned wbits = __shfl_sync(0xffffffffu, bits, src);
+        while (wbits) {
+          const int ss = ((wb + src) << 5) + __ffs(wbits) - 1;
+          wbits &= wbits - 1;
+          const int pv = lprov[ss];
+          if (pv >= 0) mmv_refresh(p, pv, ss, bmin, bmax, lane);
+        }
+      }
+      if (bits) wdirty[wb + lane] = 0u;
+    }
+    __syncwarp();
+  };
+
+  const int T = nth * ROWS;
+  const int64_t ntiles = (p.n_rows + T - 1) / T;
+  const int64_t t_per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * t_per;
+  const int64_t t1 = min(ntiles, t0 + t_per);
+  const int* kcol = (const int*)p.key_col[0];
+  int qh = 0, qn = 0;
+#pragma unroll 1
+  for (int64_t tile = t0; tile < t1; ++tile) {
+    const int64_t r0 = tile * T + ROWS * tid;
+    int kq[ROWS];
+    double vq[ROWS];
+    if (r0 + ROWS <= p.n_rows) {
+#pragma unroll
+      for (int g = 0; g < ROWS / 4; ++g) {
+        const int4 k4 = __ldcs((const int4*)kcol + (r0 >> 2) + g);
+        kq[4 * g] = k4.x; kq[4 * g + 1] = k4.y; kq[4 * g + 2] = k4.z; kq[4 * g + 3] = k4.w;
+      }
+#pragma unroll
+      for (int g = 0; g < ROWS / 2; ++g) {
+        const double2 a = __ldcs((const double2*)p.mcol + (r0 >> 1) + g);
+        vq[2 * g] = a.x; vq[2 * g + 1] = a.y;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < ROWS; ++k) {
+        const bool in = r0 + k < p.n_rows;
+        kq[k] = in ? __ldcs(kcol + r0 + k) : 0;
+        vq[k] = in ? __ldcs(p.mcol + r0 + k) : 0.0;
+      }
+    }
+    // the other CTAs' progress: pull the per-slot bound hints
+    const int hmask = (p.ablate >> 4) ? (1 << ((p.ablate >> 4) - 1)) - 1 : kMMHintEvery - 1;
+    const int nl = (p.ablate & 8) || ((tile - t0) & hmask) ? 0 : min(*(volatile int*)&misc->nlocal, Lcap);
+    for (int s2 = tid; s2 < nl; s2 += nth) {
+      const int pv = *(volatile int*)&lprov[s2];
+      if (pv < 0) continue;
+      if (MM & 2) {
+        const long long g = __ldcg(p.gbmax + pv);
+        if (g != kMaxEmpty) {
+          const double d = dec_f64(g);
+          if (!(d <= bmax[s2])) bmax[s2] = d;
+        }
+      }
+      if (MM & 1) {
+        const long long g = __ldcg(p.gbmin + pv);
+        if (g != kMinEmpty) {
+          const double d = dec_f64(g);
+          if (!(d >= bmin[s2])) bmin[s2] = d;
+        }
+      }
+    }
+    const bool full = r0 + ROWS <= p.n_rows;
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+      const int64_t r = r0 + k;
+      bool cand = false;
+      int prov = -1, s = -1;
+      if (full || r < p.n_rows) {
+        const uint32_t key = (uint32_t)kq[k] ^ 0x80000000u;  // R20 packing of one int32 column
+        const int code = local_code32(p, key, lkey, LH, lprov, Lcap, misc, bmin, bmax);
+        if (code < kOvfBase) {
+          s = code - 1;
+          prov = lprov[s];
+          atomicAdd(&lrows[s], 1u);
+          // !(v <= b): v beats the bound, or v is NaN, or the bound is NaN (admit all)
+          cand = ((MM & 2) && !(vq[k] <= bmax[s])) || ((MM & 1) && !(vq[k] >= bmin[s]));
+        } else {
+          prov = code - kOvfBase - 1;
+          if (prov >= 0) atomicAdd(&p.prov_rows[prov], 1ull);
+          cand = true;
+        }
+        if (prov < 0) cand = false;
+      }
+      const unsigned cm = __ballot_sync(0xffffffffu, cand);
+      if (cand) {
+        const int i = (qh + qn + __popc(cm & ((1u << lane) - 1u))) & (kMMQueue - 1);
+        qr[i] = r;
+        qv[i] = vq[k];
+        qp[i] = make_int2(prov, s);
+      }
+      qn += __popc(cm);
+      if (qn >= 32) {
+        __syncwarp();
+        mmv_apply<MM>(p, qr, qv, qp, qh, 32, wdirty, bmin, bmax, lprov, lane);
+        qh = (qh + 32) & (kMMQueue - 1);
+        qn -= 32;
+        __syncwarp();
+        refresh_dirty();
+      }
+    }
+  }
+  __syncwarp();
+  if (qn > 0) {
+    mmv_apply<MM>(p, qr, qv, qp, qh, qn, wdirty, bmin, bmax, lprov, lane);
     __syncwarp();
   }
   __syncthreads();
@@ -730,7 +1039,7 @@ static int build_accs(const pac_agg_spec* aggs, int n_aggs, AccSet* A, bool allo
 
 struct WsLayout {
   size_t o_gkey, o_gstate, o_ctr, o_pkey, o_prows, o_pcount, o_pisum[2], o_pfsum[2], o_pmin, o_pmax,
-      o_perm, o_sk0, o_si0, o_sk1, o_si1, o_hist, o_meta, bytes;
+      o_gbmin, o_gbmax, o_perm, o_sk0, o_si0, o_sk1, o_si1, o_hist, o_meta, bytes;
   int64_t Hcap;
   int nblocks;
 };
@@ -755,6 +1064,9 @@ static WsLayout ws_layout(const AccSet& A, int64_t G_cap) {
   for (int c = 0; c < 2; ++c) w.o_pfsum[c] = c < A.nf ? take(8 * Gc * kM) : 0;
   w.o_pmin = A.has_min ? take(8 * Gc * kM) : 0;
   w.o_pmax = A.has_max ? take(8 * Gc * kM) : 0;
+  const bool mm_only = !A.has_count;  // k_agg_minmax(_v): per-slot bound hints
+  w.o_gbmin = mm_only && A.has_min ? take(8 * Gc) : 0;
+  w.o_gbmax = mm_only && A.has_max ? take(8 * Gc) : 0;
   w.o_perm = take(4 * Gc);
   w.nblocks = (int)((Gc + kRadixChunk - 1) / kRadixChunk);
   if (Gc > kSmallSort) {
@@ -883,33 +1195,12 @@ static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, int key_
 }
 
 static MMLayout mm_layout(int64_t G_cap, int smem_max) {
-  MMLayout L{};
   int Lcap = (int)std::min<int64_t>(std::max<int64_t>(G_cap, 1), 4096);
   for (;;) {
-    L.Lcap = Lcap;
-#ifndef PAC_MM_LH
-#define PAC_MM_LH 4
-#endif
-    L.LH = (int)next_pow2(std::max(PAC_MM_LH * Lcap, 256));
-    int off = 0;
-    auto take = [&](int bytes) {
-      int o = off;
-      off += (bytes + 15) & ~15;
-      return o;
-    };
-    L.o_lkey = take(L.LH * 8);
-    L.o_lrows = take(Lcap * 4);
-    L.o_bmin = take(Lcap * 8);
-    L.o_bmax = take(Lcap * 8);
-    L.o_lstate = take(L.LH * 4);
-    L.o_lprov = take(Lcap * 4);
-    L.o_dirty = take((kThreads / 32) * ((Lcap + 31) / 32) * 4);  // per-warp dirty bitmaps
-    L.o_misc = take(sizeof(Misc));
-    L.bytes = off;
-    if (L.bytes <= smem_max || Lcap == 1) break;
+    const MMLayout L = mm_layout_for(Lcap);
+    if (L.bytes <= smem_max || Lcap == 1) return L;
     Lcap /= 2;
   }
-  return L;
 }
 
 
@@ -1167,6 +1458,8 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
   }
   p.prov_min = A.has_min ? (long long*)(ws + W.o_pmin) : nullptr;
   p.prov_max = A.has_max ? (long long*)(ws + W.o_pmax) : nullptr;
+  p.gbmin = W.o_gbmin ? (long long*)(ws + W.o_gbmin) : nullptr;
+  p.gbmax = W.o_gbmax ? (long long*)(ws + W.o_gbmax) : nullptr;
   int* perm = (int*)(ws + W.o_perm);
   int* meta = (int*)(ws + W.o_meta);
 
@@ -1184,15 +1477,29 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
   if (n_rows > 0) {
     if (!A.has_count) {
       MMLayout L = mm_layout(G_cap, smem_max);
-      e = cudaFuncSetAttribute(k_agg_minmax, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
+      // one int32 key column, hashed pu keys, 16-byte aligned columns: the vectorized instance
+      const bool vec = n_keys == 1 && keys[0].elem_bytes == 4 && d_pu_key && !getenv("PAC_NO_MMV") &&
+                       ((uintptr_t)keys[0].d_col & 15) == 0 && ((uintptr_t)A.mcol & 15) == 0;
+      const int mmk = (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0);
+      const bool r8 = false;
+      p.ablate = (getenv("PAC_MMV_NOHINT") ? 8 : 0) | (getenv("PAC_MM_HINT_LOG") ? (1 + atoi(getenv("PAC_MM_HINT_LOG"))) << 4 : 0);
+      const bool fixed = L.Lcap == 1024 && !getenv("PAC_NO_FIXED");  // e.g. BASELINE C4: 1000 groups
+      auto kern = !vec ? k_agg_minmax
+                  : fixed ? (mmk == 1 ? k_agg_minmax_v<1, 4, 1024>
+                                      : (mmk == 2 ? k_agg_minmax_v<2, 4, 1024> : k_agg_minmax_v<3, 4, 1024>))
+                          : (mmk == 1 ? k_agg_minmax_v<1, 4, 0> : (mmk == 2 ? k_agg_minmax_v<2, 4, 0> : k_agg_minmax_v<3, 4, 0>));
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
       if (e != cudaSuccess) return PAC_E_CUDA;
       int per_sm = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_agg_minmax, kThreads, L.bytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, L.bytes);
       per_sm = std::max(1, per_sm);
-      int64_t tiles = (n_rows + kThreads * kMMRows - 1) / (kThreads * kMMRows);
+      const int rows_per_thread = vec && r8 ? 8 : kMMRows;
+      int64_t tiles = (n_rows + kThreads * rows_per_thread - 1) / (kThreads * rows_per_thread);
       int grid = (int)std::min<int64_t>(tiles, (int64_t)sms * per_sm);
-      profile_begin(st, "k_agg_minmax");
-      k_agg_minmax<<<grid, kThreads, L.bytes, st>>>(p, L);
+      char kname[32];
+      snprintf(kname, sizeof(kname), vec ? "k_agg_minmax_v<%d>" : "k_agg_minmax", mmk);
+      profile_begin(st, kname);
+      kern<<<grid, kThreads, L.bytes, st>>>(p, L);
       note_launch();
       e = cudaGetLastError();
       profile_end(st);

@@ -62,6 +62,8 @@ struct AggPlan {
   double* prov_fsum[2];
   long long* prov_min;
   long long* prov_max;
+  long long* gbmin;  // per provisional slot: a recent max_j MIN_j (enc), hint for the pruning bounds
+  long long* gbmax;  // per provisional slot: a recent min_j MAX_j (enc)
   // deferred HBM tier (agg.cu k_spill_*): rows of groups without a CTA-local slot are appended
   // here (record i: sp_prov[i] = the HBM slot, or -2 when the CTA dictionary did not know it
   // (resolved from the group key sp_gkey[i] after the pass), sp_key[i] = the pu key, or the
@@ -165,6 +167,8 @@ __device__ __forceinline__ void init_prov_slot(const AggPlan& p, int prov, uint6
   for (int c = 0; c < p.nf; ++c) fill_world_row(p.prov_fsum[c] + b, 0);  // +0.0
   if (p.has_min) fill_world_row(p.prov_min + b, kMinEmpty);
   if (p.has_max) fill_world_row(p.prov_max + b, kMaxEmpty);
+  if (p.gbmin) p.gbmin[prov] = kMinEmpty;
+  if (p.gbmax) p.gbmax[prov] = kMaxEmpty;
 }
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* a) {
