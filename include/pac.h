@@ -364,6 +364,26 @@ int pac_join_table_status(const void* d_table, pac_stream_t stream);
 int pac_join_mask(const void* const* d_tables, int k, const int64_t* d_fk, int64_t n, uint64_t salt,
                   uint64_t* d_mask, int64_t* d_pu_key, pac_stream_t stream);
 
+/* ------------------------------------------------------------------ approximate SUM (§8 f3)
+ * P:L1783-1803 (§5 "Approximation", "Two-sided SUM"); readings R35 (two-sided), R36 (single-
+ * sided).  Ungrouped 64-world SUM of an int64 column with the paper's approximate state: per
+ * world and side 25 levels of 16-bit counters, level k of weight 2^(4k); a value v != 0 of a row
+ * in world j goes to side pos (v > 0) or neg (stored negated), is routed to level
+ * l = floor((msb(|v|) - 8) / 4) (0 below 2^8) and adds |v| >> 4l; on overflow the counter's upper
+ * 12 bits cascade into the next level (C[k+1] += C[k] >> 4) and its low 4 bits are dropped.
+ * two_sided == 0: Table 1's "Single Sum" (R36): one state fed the value's 64-bit two's-complement
+ * pattern (routed by its msb), decoded modulo 2^64 as a signed int64.  Order (R35): rows in row order inside blocks of block_rows rows, block states
+ * combined in block order -- the result is a deterministic function of (rows, block_rows).
+ * Masks: exactly one of d_pu_key (hashed with salt, = pac_mask) and d_mask.
+ * Outputs: d_counters [2][64][25] uint16 (side, world, level; single-sided: side 1 zeros);
+ * d_y [64] = 2 * (dec(pos) - dec(neg)) (R7; single-sided 2 * (int64)(dec mod 2^64)),
+ * dec(C) = sum_k C[k] 2^(4k) in double.  Workspace: pac_approx_sum_workspace_size bytes.
+ * Errors: PAC_E_INVAL, PAC_E_WORKSPACE, PAC_E_CUDA. */
+int pac_approx_sum_workspace_size(int64_t n_rows, int64_t block_rows, size_t* bytes);
+int pac_approx_sum(const int64_t* d_pu_key, const uint64_t* d_mask, uint64_t salt, const int64_t* d_values,
+                   int64_t n_rows, int32_t two_sided, int64_t block_rows, uint16_t* d_counters, double* d_y,
+                   void* d_ws, size_t ws_bytes, pac_stream_t stream);
+
 /* ------------------------------------------------------------------ runtime / profiling
  * Number of kernels this library has launched since load (all entry points). */
 uint64_t pac_launch_count(void);

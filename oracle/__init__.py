@@ -475,3 +475,21 @@ def finalize128(seed: int, B: float, jstar: int, P: np.ndarray, table: dict, rou
                             _ptr(table["rows"]), _ptr(count), wptr, int(round_), _ptr(release), _ptr(is_null),
                             _ptr(flags), _ptr(delta))
     return release, is_null, flags, delta, P
+
+
+# ------------------------------------------------------------------ approximate SUM (§8 f3)
+AL = 25  # levels
+
+
+def approx_sum(masks: np.ndarray, values: np.ndarray, block_rows: int = 65536, two_sided: bool = True):
+    """Approximate (two-sided) SUM of an ungrouped column over the 64 worlds (R35/R36).  Returns
+    (counters uint16 [2, 64, 25] -- single-sided: int16 view of [0], y[64] released scale)."""
+    masks = np.ascontiguousarray(masks, dtype=np.uint64)
+    values = np.ascontiguousarray(values, dtype=np.int64)
+    cnt = np.zeros((2, M, AL), dtype=np.uint16)
+    y = np.zeros(M, dtype=np.float64)
+    L = _load()
+    L.orc_approx_sum.argtypes = [_P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int, _P, _P]
+    L.orc_approx_sum(_ptr(masks), masks.shape[0], _ptr(values), int(block_rows), 1 if two_sided else 0,
+                     _ptr(cnt), _ptr(y))
+    return cnt, y

@@ -938,3 +938,84 @@ void orc_finalize128(uint64_t seed, double B, int jstar, double* P, int64_t G, i
     }
   }
 }
+
+/* ------------------------------------------------------------------ approximate SUM (§8 f3)
+ * P:L1783-1803 (§5 "Approximation", "Two-sided SUM"); readings DESIGN.md R35-R36.
+ * Per world and side, 25 levels of 16-bit counters C[k] of weight 2^(4k).  A value v != 0 of a
+ * row in world j goes to side pos (v > 0) or neg (v < 0, stored negated); with
+ * a = |v|, msb = index of its highest set bit, it is routed to level
+ *   l(v) = floor((msb - 8) / 4)   (0 for msb < 8, capped at 24)
+ * and adds c = a >> 4l.  Overflow (C[l] + c > 0xFFFF): "only the upper 12 bits of each counter
+ * cascade: C[k+1] += C[k] >> 4" -- the counter's low 4 bits are dropped and it restarts
+ * at 0 (R35), recursively upward, then c is added.  Result (R7): 2 * (dec(pos) - dec(neg)),
+ * dec(C) = sum_k C[k] 2^(4k).  Single-sided variant (Table 1's "Single Sum", R36): one state fed
+ * the value's 64-bit two's-complement pattern u = (uint64)v -- routed by msb(u), adding u >> 4l --
+ * and decoded modulo 2^64 as a signed int64 (a negative value has msb 63 and loses its low 52
+ * bits: the failure Table 1 shows on negative_mixed, which the second, negated state avoids).
+ * Execution order (R35): rows in row order within consecutive blocks of block_rows rows (the
+ * thread-local states of P:L1966), block states combined in block order by adding each level of
+ * the next block's state into the running state with the same add-with-cascade rule. */
+#define ORC_AL 25
+
+static void approx_add_u(uint16_t* C, int k, uint32_t c) {
+  if (k >= ORC_AL) return; /* beyond 112 bits: out of contract (R35) */
+  if ((uint32_t)C[k] + c > 0xFFFFu) {
+    approx_add_u(C, k + 1, (uint32_t)(C[k] >> 4));
+    C[k] = 0;
+  }
+  C[k] = (uint16_t)(C[k] + c);
+}
+
+static int approx_level(uint64_t a) {
+  int msb = 63;
+  while (msb > 0 && ((a >> msb) & 1u) == 0) msb--;
+  int l = msb < 8 ? 0 : (msb - 8) / 4;
+  return l > ORC_AL - 1 ? ORC_AL - 1 : l;
+}
+
+/* counters: [2][64][25] uint16 (side 0 = pos, 1 = neg; single-sided: side 0 only).  y[64] = the
+ * released-scale world values 2 * (dec(pos) - dec(neg)), resp. 2 * (int64)(dec mod 2^64). */
+void orc_approx_sum(const uint64_t* masks, int64_t n, const int64_t* values, int64_t block_rows, int two_sided,
+                    uint16_t* counters, double* y) {
+  const size_t nc = (size_t)2 * ORC_M * ORC_AL;
+  uint16_t* run = (uint16_t*)calloc(nc, sizeof(uint16_t));
+  uint16_t* blk = (uint16_t*)calloc(nc, sizeof(uint16_t));
+  for (int64_t b0 = 0; b0 < n; b0 += block_rows) {
+    memset(blk, 0, nc * sizeof(uint16_t));
+    int64_t b1 = b0 + block_rows < n ? b0 + block_rows : n;
+    for (int64_t r = b0; r < b1; r++) {
+      int64_t v = values[r];
+      if (v == 0 || masks[r] == 0) continue;
+      uint64_t a = !two_sided ? (uint64_t)v : (v > 0 ? (uint64_t)v : (uint64_t)0 - (uint64_t)v);
+      int l = approx_level(a);
+      uint32_t c = (uint32_t)(a >> (4 * l));
+      int side = two_sided && v < 0 ? 1 : 0;
+      for (int j = 0; j < ORC_M; j++) {
+        if (((masks[r] >> j) & 1u) == 0) continue;
+        approx_add_u(blk + ((size_t)side * ORC_M + j) * ORC_AL, l, c);
+      }
+    }
+    /* combine the block into the running state, level by level, block order */
+    for (int s = 0; s < (two_sided ? 2 : 1); s++)
+      for (int j = 0; j < ORC_M; j++)
+        for (int k = 0; k < ORC_AL; k++) {
+          size_t o = ((size_t)s * ORC_M + j) * ORC_AL;
+          approx_add_u(run + o, k, blk[o + k]);
+        }
+  }
+  memcpy(counters, run, nc * sizeof(uint16_t));
+  for (int j = 0; j < ORC_M; j++) {
+    if (two_sided) {
+      double d = 0.0, sc = 1.0;
+      for (int k = 0; k < ORC_AL; k++, sc *= 16.0)
+        d += ((double)run[(size_t)j * ORC_AL + k] - (double)run[((size_t)ORC_M + j) * ORC_AL + k]) * sc;
+      y[j] = 2.0 * d;
+    } else {
+      uint64_t u = 0; /* decode modulo 2^64 (levels >= 16 vanish) */
+      for (int k = 0; k < 16; k++) u += (uint64_t)run[(size_t)j * ORC_AL + k] << (4 * k);
+      y[j] = 2.0 * (double)(int64_t)u;
+    }
+  }
+  free(run);
+  free(blk);
+}

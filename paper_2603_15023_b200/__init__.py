@@ -13,3 +13,4 @@ from .api import (CMP_EQ, CMP_GE, CMP_GT, CMP_LE, CMP_LT, OP_ADD, OP_DIV, OP_MAX
 from .api import JoinTable, join_mask  # noqa: F401
 from .api import Aggregator128, mask128  # noqa: F401
 from .api import MergeBuffers, merge_pack, merge_unpack  # noqa: F401
+from .api import approx_sum  # noqa: F401

@@ -105,6 +105,9 @@ def lib() -> ctypes.CDLL:
         "pac_profile_read": (ctypes.c_int, [_P, _P]),
         "pac_profile_last_kernel": (ctypes.c_char_p, []),
         "pac_merge_sizes": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int64, _P, _P, _P]),
+        "pac_approx_sum_workspace_size": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, _P]),
+        "pac_approx_sum": (ctypes.c_int, [_P, _P, ctypes.c_uint64, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64,
+                                          _P, _P, _P, ctypes.c_size_t, _P]),
         "pac_merge_pack": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int64, _P, _P, _P, _P]),
         "pac_merge_unpack": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int64, _P, _P, _P, _P]),
         "pac_version": (ctypes.c_char_p, []),
@@ -132,4 +135,5 @@ def exported_symbols() -> list:
             "pac_select", "pac_select_cmp", "pac_filter", "pac_filter_cmp", "pac_join_table_bytes",
             "pac_join_build", "pac_join_table_status", "pac_join_mask", "pac_launch_count",
             "pac_profile_enable", "pac_profile_read", "pac_profile_last_kernel", "pac_version",
-            "pac_merge_sizes", "pac_merge_pack", "pac_merge_unpack"]
+            "pac_merge_sizes", "pac_merge_pack", "pac_merge_unpack", "pac_approx_sum_workspace_size",
+            "pac_approx_sum"]

@@ -531,6 +531,24 @@ def join_mask(tables: Sequence[JoinTable], fk: torch.Tensor, salt: int, want_pu:
     return (mask, pu) if want_pu else mask
 
 
+# ------------------------------------------------------------------ approximate SUM (§8 f3)
+def approx_sum(values: torch.Tensor, pu_key: Optional[torch.Tensor] = None, mask: Optional[torch.Tensor] = None,
+               salt: int = 0, two_sided: bool = True, block_rows: int = 65536):
+    """pac_approx_sum (R35/R36): ungrouped approximate 64-world SUM.  Returns (counters uint16
+    [2, 64, 25] as int16 bit patterns in an int16 tensor, y float64 [64])."""
+    _require_cuda(values, pu_key, mask)
+    n = values.numel()
+    nb = ctypes.c_size_t()
+    check("pac_approx_sum_workspace_size", L.lib().pac_approx_sum_workspace_size(n, int(block_rows), ctypes.byref(nb)))
+    ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=values.device)
+    cnt = torch.zeros(2, PAC_M, 25, dtype=torch.int16, device=values.device)
+    y = torch.empty(PAC_M, dtype=torch.float64, device=values.device)
+    check("pac_approx_sum", L.lib().pac_approx_sum(_ptr(pu_key), _ptr(mask), salt & 0xFFFFFFFFFFFFFFFF, _ptr(values), n,
+                                                    1 if two_sided else 0, int(block_rows), _ptr(cnt), _ptr(y), _ptr(ws),
+                                                    nb.value, _stream(values.device)))
+    return cnt, y
+
+
 # ------------------------------------------------------------------ runtime
 def launch_count() -> int:
     return int(L.lib().pac_launch_count())

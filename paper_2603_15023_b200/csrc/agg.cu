@@ -1181,7 +1181,8 @@ static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, int key_
   const int want_tm = (want > 64 && want <= kTmFixedSlots && 4 * (kTmFixedSlots / 16) * wps <= kTmCols)
                           ? kTmFixedSlots : want;
   if (want > 32 && 4 * ((want_tm + 15) / 16) * wps <= kTmCols && !getenv("PAC_NO_TM")) {
-    for (int T : {2048, 1024}) {
+    const int Tx = getenv("PAC_TM_T") ? atoi(getenv("PAC_TM_T")) : 2048;  // experiments
+    for (int T : {Tx, 2048, 1024}) {
       SmemLayout L = make_layout(A, T, want_tm, key_bytes, true);
       if (L.bytes <= smem_max) {
         *out = L;
