@@ -1141,7 +1141,8 @@ static SmemLayout make_layout(const AccSet& A, int T, int Lcap, int key_bytes = 
 // fit.  PAC_TILE=512|1024 forces the tile size (experiments).
 static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, int key_bytes, SmemLayout* out) {
   // small tables get kFixedSlots local slots: the compile-time-layout kernel instance
-  const int want = (int)std::min<int64_t>(std::max<int64_t>(G_cap, (int64_t)kFixedSlots), 256);
+  const int cap = getenv("PAC_LCAP_MAX") ? atoi(getenv("PAC_LCAP_MAX")) : 256;  // experiments
+  const int want = (int)std::min<int64_t>(std::max<int64_t>(G_cap, (int64_t)kFixedSlots), cap);
   if (getenv("PAC_FORCE_TM")) {  // experiments: the TMEM-table kernel at any slot count
     const int T = atoi(getenv("PAC_FORCE_TM")) >= 1024 ? atoi(getenv("PAC_FORCE_TM")) : 2048;
     SmemLayout L = make_layout(A, T, want, key_bytes, true);
