@@ -162,7 +162,7 @@ class PacTable:
             "G": G,
             "keys": as_u64(self.group_key[:G]),
             "rows": self.rows[:G].cpu().numpy(),
-            "K": as_u64(self.presence[:G]) if self.m == PAC_M else as_u64(self.presence[:G].contiguous()).reshape(G, -1),
+            "K": as_u64(self.presence[:G]) if self.m == PAC_M else as_u64(self.presence[:G].contiguous()).reshape(G, self.m // PAC_M),
             "count": None if self.count is None else self.count[:G].cpu().numpy(),
             "world": [None if w is None else w[:G].cpu().numpy() for w in self.world],
             "kinds": list(self.kinds),

@@ -970,6 +970,47 @@ __global__ void k_gather(AggPlan p, const int* Gdev, const int* perm, pac_table 
   }
 }
 
+// m = 128 tables (native path, agg128.cu): one warp per output group, lane j -> worlds j + 32 h
+__global__ void k_gather128(AggPlan p, const int* Gdev, const int* perm, pac_table out, int n_aggs,
+                            const int* src_kind, const int* src_idx) {
+  const int G = *Gdev;
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int rank = blockIdx.x * wpb + (threadIdx.x >> 5); rank < G; rank += gridDim.x * wpb) {
+    const int prov = perm[rank];
+    const size_t pb = (size_t)prov * 2 * kM, ob = (size_t)rank * 2 * kM;
+    uint64_t K0 = 0, K1 = 0;  // presence of worlds 0..63 and 64..127 (R5)
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const unsigned long long c = p.prov_count[pb + lane + 32 * h];
+      out.d_count[ob + lane + 32 * h] = (int64_t)c;
+      const uint64_t bal = (uint64_t)__ballot_sync(0xffffffffu, c != 0) << (32 * (h & 1));
+      if (h < 2) K0 |= bal; else K1 |= bal;
+    }
+    for (int a = 0; a < n_aggs; ++a) {
+      void* w = out.d_world[a];
+      if (!w) continue;
+      const int kd = src_kind[a], ix = src_idx[a];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int j = lane + 32 * h;
+        if (kd == 1) ((int64_t*)w)[ob + j] = (int64_t)p.prov_isum[ix][pb + j];
+        else if (kd == 2) ((double*)w)[ob + j] = p.prov_fsum[ix][pb + j];
+      }
+    }
+    if (lane == 0) {
+      out.d_group_key[rank] = p.prov_key[prov];
+      out.d_rows[rank] = (int64_t)p.prov_rows[prov];
+      out.d_presence[2 * rank] = K0;
+      out.d_presence[2 * rank + 1] = K1;
+      if (p.ni > 0) {  // R15 overflow check, as k_gather
+        const unsigned long long ma = *p.gmaxabs, rows = p.prov_rows[prov];
+        if (ma && rows > (0x7FFFFFFFFFFFFFFFull / ma)) atomicExch(out.d_status, PAC_E_OVERFLOW);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host helpers
 static int64_t next_pow2(int64_t v) {
   int64_t p = 1;
@@ -1044,7 +1085,8 @@ struct WsLayout {
   int nblocks;
 };
 
-static WsLayout ws_layout(const AccSet& A, int64_t G_cap) {
+// worlds: words per provisional world row (64; 128 for the native m = 128 path)
+static WsLayout ws_layout(const AccSet& A, int64_t G_cap, int worlds = kM) {
   WsLayout w{};
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -1059,11 +1101,11 @@ static WsLayout ws_layout(const AccSet& A, int64_t G_cap) {
   w.o_ctr = take(64);  // gcounter, Gdev, gmaxabs, dbg[2], spill records reserved / grouped, key OR / AND
   w.o_pkey = take(8 * Gc);
   w.o_prows = take(8 * Gc);
-  w.o_pcount = A.has_count ? take(8 * Gc * kM) : 0;
-  for (int c = 0; c < 2; ++c) w.o_pisum[c] = c < A.ni ? take(8 * Gc * kM) : 0;
-  for (int c = 0; c < 2; ++c) w.o_pfsum[c] = c < A.nf ? take(8 * Gc * kM) : 0;
-  w.o_pmin = A.has_min ? take(8 * Gc * kM) : 0;
-  w.o_pmax = A.has_max ? take(8 * Gc * kM) : 0;
+  w.o_pcount = A.has_count ? take(8 * Gc * worlds) : 0;
+  for (int c = 0; c < 2; ++c) w.o_pisum[c] = c < A.ni ? take(8 * Gc * worlds) : 0;
+  for (int c = 0; c < 2; ++c) w.o_pfsum[c] = c < A.nf ? take(8 * Gc * worlds) : 0;
+  w.o_pmin = A.has_min ? take(8 * Gc * worlds) : 0;
+  w.o_pmax = A.has_max ? take(8 * Gc * worlds) : 0;
   const bool mm_only = !A.has_count;  // k_agg_minmax(_v): per-slot bound hints
   w.o_gbmin = mm_only && A.has_min ? take(8 * Gc) : 0;
   w.o_gbmax = mm_only && A.has_max ? take(8 * Gc) : 0;
@@ -1392,37 +1434,21 @@ extern "C" int pac_agg_workspace_size_rows(const pac_agg_spec* aggs, int n_aggs,
   return PAC_OK;
 }
 
-extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, uint64_t salt,
-                               const pac_key_col* keys, int n_keys, const pac_agg_spec* aggs, int n_aggs,
-                               int64_t n_rows, const pac_table* out, int64_t G_cap, void* d_ws,
-                               size_t ws_bytes, pac_stream_t stream) {
-  if (n_rows < 0 || !out || G_cap < 1 || (out->m != 0 && out->m != 64)) return PAC_E_INVAL;  // m = 128: pac_agg_grouped128
-  // exactly one mask source (an empty input may arrive as NULL pointers)
-  if (d_pu_key && d_mask) return PAC_E_INVAL;
-  if (!d_pu_key && !d_mask && n_rows > 0) return PAC_E_INVAL;
+// group-key columns: at most PAC_MAX_KEYS of 1, 2, 4 or 8 bytes, packed width <= 8 bytes
+static int check_keys(const pac_key_col* keys, int n_keys, int64_t n_rows, int* width) {
   if (n_keys < 0 || n_keys > PAC_MAX_KEYS || (n_keys > 0 && !keys)) return PAC_E_INVAL;
-  int width = 0;
+  *width = 0;
   for (int c = 0; c < n_keys; ++c) {
-    int w = keys[c].elem_bytes;
+    const int w = keys[c].elem_bytes;
     if ((w != 1 && w != 2 && w != 4 && w != 8) || (!keys[c].d_col && n_rows > 0)) return PAC_E_INVAL;
-    width += w;
+    *width += w;
   }
-  if (width > 8) return PAC_E_INVAL;
-  AccSet A;
-  int rc = build_accs(aggs, n_aggs, &A, n_rows == 0);
-  if (rc) return rc;
-  if (!out->d_num_groups || !out->d_status || !out->d_group_key || !out->d_rows || !out->d_presence)
-    return PAC_E_INVAL;
-  if (A.has_count && !out->d_count) return PAC_E_INVAL;
-  for (int a = 0; a < n_aggs; ++a)
-    if (aggs[a].kind != PAC_COUNT && !out->d_world[a]) return PAC_E_INVAL;
-  WsLayout W = ws_layout(A, G_cap);
-  if (!d_ws || ws_bytes < W.bytes) return PAC_E_WORKSPACE;
-  int sms = 148, smem_max = 0;
-  if (device_info(&sms, &smem_max) != PAC_OK) return PAC_E_CUDA;
-  cudaStream_t st = (cudaStream_t)stream;
-  char* ws = (char*)d_ws;
+  return *width > 8 ? PAC_E_INVAL : PAC_OK;
+}
 
+// The plan fields every aggregation path shares (inputs, accumulator set, workspace pointers).
+static AggPlan make_plan(const int64_t* d_pu_key, const uint64_t* d_mask, uint64_t salt, const pac_key_col* keys,
+                         int n_keys, int64_t n_rows, const AccSet& A, const WsLayout& W, char* ws, int64_t G_cap) {
   AggPlan p{};
   p.n_rows = n_rows;
   p.pu_key = (const long long*)d_pu_key;
@@ -1447,7 +1473,6 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
   p.gstate = (int*)(ws + W.o_gstate);
   p.hmask = (uint32_t)(W.Hcap - 1);
   p.gcounter = (int*)(ws + W.o_ctr);
-  int* Gdev = (int*)(ws + W.o_ctr + 4);
   p.gmaxabs = (unsigned long long*)(ws + W.o_ctr + 8);
   p.dbg = (unsigned long long*)(ws + W.o_ctr + 16);
   p.G_cap = G_cap;
@@ -1462,9 +1487,12 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
   p.prov_max = A.has_max ? (long long*)(ws + W.o_pmax) : nullptr;
   p.gbmin = W.o_gbmin ? (long long*)(ws + W.o_gbmin) : nullptr;
   p.gbmax = W.o_gbmax ? (long long*)(ws + W.o_gbmax) : nullptr;
-  int* perm = (int*)(ws + W.o_perm);
-  int* meta = (int*)(ws + W.o_meta);
+  return p;
+}
 
+// Clears the workspace dictionary and counters and uploads the output-column map (async on st).
+static int plan_reset(const AccSet& A, const WsLayout& W, char* ws, int n_aggs, cudaStream_t st) {
+  int* meta = (int*)(ws + W.o_meta);
   if (cudaMemsetAsync(ws + W.o_gstate, 0, 4 * W.Hcap, st) != cudaSuccess) return PAC_E_CUDA;
   if (cudaMemsetAsync(ws + W.o_ctr, 0, 64, st) != cudaSuccess) return PAC_E_CUDA;
   int hmeta[2 * PAC_MAX_AGGS];
@@ -1474,7 +1502,40 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
   }
   if (cudaMemcpyAsync(meta, hmeta, sizeof(hmeta), cudaMemcpyHostToDevice, st) != cudaSuccess)
     return PAC_E_CUDA;
+  return PAC_OK;
+}
 
+extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, uint64_t salt,
+                               const pac_key_col* keys, int n_keys, const pac_agg_spec* aggs, int n_aggs,
+                               int64_t n_rows, const pac_table* out, int64_t G_cap, void* d_ws,
+                               size_t ws_bytes, pac_stream_t stream) {
+  if (n_rows < 0 || !out || G_cap < 1 || (out->m != 0 && out->m != 64)) return PAC_E_INVAL;  // m = 128: pac_agg_grouped128
+  // exactly one mask source (an empty input may arrive as NULL pointers)
+  if (d_pu_key && d_mask) return PAC_E_INVAL;
+  if (!d_pu_key && !d_mask && n_rows > 0) return PAC_E_INVAL;
+  int width = 0;
+  if (check_keys(keys, n_keys, n_rows, &width) != PAC_OK) return PAC_E_INVAL;
+  AccSet A;
+  int rc = build_accs(aggs, n_aggs, &A, n_rows == 0);
+  if (rc) return rc;
+  if (!out->d_num_groups || !out->d_status || !out->d_group_key || !out->d_rows || !out->d_presence)
+    return PAC_E_INVAL;
+  if (A.has_count && !out->d_count) return PAC_E_INVAL;
+  for (int a = 0; a < n_aggs; ++a)
+    if (aggs[a].kind != PAC_COUNT && !out->d_world[a]) return PAC_E_INVAL;
+  WsLayout W = ws_layout(A, G_cap);
+  if (!d_ws || ws_bytes < W.bytes) return PAC_E_WORKSPACE;
+  int sms = 148, smem_max = 0;
+  if (device_info(&sms, &smem_max) != PAC_OK) return PAC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = (char*)d_ws;
+
+  AggPlan p = make_plan(d_pu_key, d_mask, salt, keys, n_keys, n_rows, A, W, ws, G_cap);
+  int* Gdev = (int*)(ws + W.o_ctr + 4);
+  int* perm = (int*)(ws + W.o_perm);
+  int* meta = (int*)(ws + W.o_meta);
+
+  if (int rc2 = plan_reset(A, W, ws, n_aggs, st)) return rc2;
   cudaError_t e = cudaSuccess;
   if (n_rows > 0) {
     if (!A.has_count) {
@@ -1644,6 +1705,99 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
   }
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
 }
+
+namespace pac {
+// ------------------------------------------------------------------ native m = 128 (agg128.cu)
+int tiles128_smem(int ni, int nf, int Lcap, int raw_bytes);
+int tiles128_rows();
+cudaError_t launch_tiles128(const AggPlan& p, int Lcap, int sms, cudaStream_t st);
+
+constexpr int kNative128Slots = 32;  // k_agg_tiles128: one warp scans the slot histogram
+
+// The single-pass m = 128 kernel applies: COUNT / SUM / AVG aggregates, G_cap <= 32 (every group a
+// CTA-local slot), and its CTA table fits shared memory.  PAC_NO_NATIVE128=1 forces the 3-pass path.
+bool agg128_native_ok(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, const pac_key_col* keys, int n_keys,
+                      bool masked) {
+  if (getenv("PAC_NO_NATIVE128") || G_cap < 1 || G_cap > kNative128Slots) return false;
+  int width = 0;
+  if (check_keys(keys, n_keys, 0, &width) != PAC_OK) return false;
+  AccSet A;
+  if (build_accs(aggs, n_aggs, &A, true, true) != PAC_OK || A.has_min || A.has_max) return false;
+  int sms = 148, smem_max = 0;
+  if (device_info(&sms, &smem_max) != PAC_OK) return false;
+  return tiles128_smem(A.ni, A.nf, (int)G_cap, 0) <= smem_max;  // staging is dropped when it does not fit
+}
+
+// workspace of the native path (0 when the aggregate list is invalid)
+size_t agg128_native_ws(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap) {
+  AccSet A;
+  if (G_cap < 1 || build_accs(aggs, n_aggs, &A, true, true) != PAC_OK) return 0;
+  return ws_layout(A, G_cap, 2 * kM).bytes;
+}
+
+int agg128_native(const int64_t* d_pu_key, const uint64_t* d_mask2, uint64_t salt, const pac_key_col* keys,
+                  int n_keys, const pac_agg_spec* aggs, int n_aggs, int64_t n_rows, const pac_table* out,
+                  int64_t G_cap, void* d_ws, size_t ws_bytes, pac_stream_t stream) {
+  int width = 0;
+  if (check_keys(keys, n_keys, n_rows, &width) != PAC_OK) return PAC_E_INVAL;
+  AccSet A;
+  int rc = build_accs(aggs, n_aggs, &A, n_rows == 0);
+  if (rc) return rc;
+  if (A.has_min || A.has_max || !out->d_count) return PAC_E_INVAL;
+  for (int a = 0; a < n_aggs; ++a)
+    if (aggs[a].kind != PAC_COUNT && !out->d_world[a]) return PAC_E_INVAL;
+  const WsLayout W = ws_layout(A, G_cap, 2 * kM);
+  if (!d_ws || ws_bytes < W.bytes) return PAC_E_WORKSPACE;
+  int sms = 148, smem_max = 0;
+  if (device_info(&sms, &smem_max) != PAC_OK) return PAC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = (char*)d_ws;
+  AggPlan p = make_plan(d_pu_key, d_mask2, salt, keys, n_keys, n_rows, A, W, ws, G_cap);
+  p.m128 = 1;
+  {  // raw columns staged per tile by TMA (Cols128 order)
+    const int T = tiles128_rows();
+    int off = 0;
+    bool aligned = true;
+    auto add = [&](const void* col, int eb) {
+      p.raw_src[p.nraw] = col;
+      p.raw_eb[p.nraw] = eb;
+      p.raw_off[p.nraw] = off;
+      off += (T * eb + 15) & ~15;
+      aligned = aligned && (((uintptr_t)col) & 15) == 0;
+      ++p.nraw;
+    };
+    p.nraw = 0;
+    add(d_mask2 ? (const void*)d_mask2 : (const void*)d_pu_key, d_mask2 ? 16 : 8);
+    for (int c = 0; c < A.ni; ++c) add(A.icol[c], 8);
+    for (int c = 0; c < A.nf; ++c) add(A.fcol[c], 8);
+    for (int c = 0; c < n_keys; ++c) add(keys[c].d_col, keys[c].elem_bytes);
+    p.raw_bytes = off;
+    p.tma_ok = (aligned && !getenv("PAC_NO_TMA")) ? 1 : 0;
+    if (tiles128_smem(A.ni, A.nf, (int)G_cap, off) > smem_max) {  // large CTA tables: loads, no staging
+      p.raw_bytes = 0;
+      p.tma_ok = 0;
+    }
+  }
+  int* Gdev = (int*)(ws + W.o_ctr + 4);
+  int* perm = (int*)(ws + W.o_perm);
+  int* meta = (int*)(ws + W.o_meta);
+  if ((rc = plan_reset(A, W, ws, n_aggs, st)) != PAC_OK) return rc;
+  if (n_rows > 0) {
+    char kname[48];
+    snprintf(kname, sizeof(kname), "k_agg_tiles128<%d,%d>", A.ni, A.nf);
+    profile_begin(st, kname);
+    const cudaError_t e = launch_tiles128(p, (int)G_cap, sms, st);
+    profile_end(st);
+    if (e != cudaSuccess) return PAC_E_CUDA;
+  }
+  k_finish_count<<<1, 1, 0, st>>>(p, n_keys, out->d_num_groups, out->d_status, Gdev);
+  k_sort_small<<<1, 1024, 0, st>>>(p.prov_key, Gdev, perm);
+  k_gather128<<<std::max(1, (int)((G_cap + 7) / 8)), 256, 0, st>>>(p, Gdev, perm, *out, n_aggs, meta,
+                                                                   meta + PAC_MAX_AGGS);
+  for (int q = 0; q < 3; ++q) note_launch();
+  return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
+}
+}  // namespace pac
 
 extern "C" int pac_table_check(const pac_table* t, int64_t* h_num_groups, pac_stream_t stream) {
   if (!t || !t->d_num_groups || !t->d_status) return PAC_E_INVAL;

@@ -76,6 +76,7 @@ struct AggPlan {
   unsigned long long* sp_key;
   unsigned long long* sp_val;
   int* sp_cnt;  // [G_cap] records per provisional slot
+  int m128;     // 1: provisional world rows are 128 words (k_agg_tiles128, agg128.cu)
 };
 
 struct SmemLayout {
@@ -161,12 +162,15 @@ __device__ __forceinline__ void fill_world_row(void* dst, long long v) {
 __device__ __forceinline__ void init_prov_slot(const AggPlan& p, int prov, uint64_t key) {
   p.prov_key[prov] = key;
   p.prov_rows[prov] = 0;
-  const size_t b = (size_t)prov * kM;
-  if (p.has_count) fill_world_row(p.prov_count + b, 0);
-  for (int c = 0; c < p.ni; ++c) fill_world_row(p.prov_isum[c] + b, 0);
-  for (int c = 0; c < p.nf; ++c) fill_world_row(p.prov_fsum[c] + b, 0);  // +0.0
-  if (p.has_min) fill_world_row(p.prov_min + b, kMinEmpty);
-  if (p.has_max) fill_world_row(p.prov_max + b, kMaxEmpty);
+  const int halves = p.m128 ? 2 : 1;
+  for (int h = 0; h < halves; ++h) {
+    const size_t b = ((size_t)prov * halves + h) * kM;
+    if (p.has_count) fill_world_row(p.prov_count + b, 0);
+    for (int c = 0; c < p.ni; ++c) fill_world_row(p.prov_isum[c] + b, 0);
+    for (int c = 0; c < p.nf; ++c) fill_world_row(p.prov_fsum[c] + b, 0);  // +0.0
+    if (p.has_min) fill_world_row(p.prov_min + b, kMinEmpty);
+    if (p.has_max) fill_world_row(p.prov_max + b, kMaxEmpty);
+  }
   if (p.gbmin) p.gbmin[prov] = kMinEmpty;
   if (p.gbmax) p.gbmax[prov] = kMaxEmpty;
 }

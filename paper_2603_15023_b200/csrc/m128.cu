@@ -10,52 +10,17 @@
 //                  aggregations -- the paper's "double the cost")
 //      k_merge128  lays L and H out on N's groups: world j < 64 from L, j >= 64 from H; groups
 //                  absent from L or H take the empty state (count 0, sums 0, MIN +inf, MAX -inf)
+//  * native path (agg.cu agg128_native, kernel k_agg_tiles128 in agg128.cu): for COUNT / SUM / AVG
+//    with G_cap <= 32, one pass that hashes both words of a row and updates all 128 worlds
+//    (PAC_NO_NATIVE128=1 forces the three passes)
 //    The finalize over 128 worlds is pac_finalize with an m = 128 session (session.cu).
 #include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
+#include "hash128.cuh"
 
 namespace pac {
-
-constexpr int kM2 = 128;
-constexpr uint64_t kHi128 = 0x6A09E667F3BCC909ull;
-
-// R28: rejection flips over 128 positions with 7-bit draws (9 per word), branch-free per word
-__device__ __forceinline__ void draw_word128(uint64_t w, uint64_t& c0, uint64_t& c1, int& k) {
-#pragma unroll
-  for (int t = 0; t < 9; ++t) {
-    const uint32_t p = (uint32_t)(w >> (7 * t)) & 127u;
-    const uint64_t oh = (uint64_t)(uint32_t)min(k, 1) << (p & 63u);
-    const uint64_t o0 = p < 64 ? oh : 0ull, o1 = p < 64 ? 0ull : oh;
-    const bool hit = ((c0 & o0) | (c1 & o1)) != 0ull;
-    c0 &= ~o0;
-    c1 &= ~o1;
-    k -= hit ? 1 : 0;
-  }
-}
-
-__device__ __forceinline__ void pac_hash128_dev(uint64_t key, uint64_t salt, uint64_t& lo, uint64_t& hi) {
-  const uint64_t x0 = fmix64(key ^ salt);
-  const uint64_t x1 = fmix64(x0 ^ kHi128);
-  const int c = __popcll(x0) + __popcll(x1);
-  const bool maj = c > 64;
-  int k = maj ? c - 64 : 64 - c;
-  uint64_t c0 = maj ? x0 : ~x0, c1 = maj ? x1 : ~x1;  // positions carrying the majority value
-  uint64_t w = fmix64(x0 ^ x1 ^ kDrawSeed);
-  draw_word128(w, c0, c1, k);
-#pragma unroll 1
-  for (int word = 1; word < 64 && k > 0; ++word) {
-    w = fmix64(w + kDrawStep);
-    draw_word128(w, c0, c1, k);
-  }
-  while (k > 0) {  // safety net of R2 / R28 (never reached in practice)
-    if (c0) c0 &= c0 - 1; else c1 &= c1 - 1;
-    --k;
-  }
-  lo = maj ? c0 : ~c0;
-  hi = maj ? c1 : ~c1;
-}
 
 __global__ void __launch_bounds__(256) k_mask128(const long long* __restrict__ key, int64_t n, uint64_t salt,
                                                  unsigned long long* __restrict__ out) {
@@ -139,6 +104,14 @@ __global__ void k_merge128(pac_table N, pac_table L, pac_table H, int64_t G_cap,
     *out.d_status = sn ? sn : (sl ? sl : sh);
   }
 }
+
+// native single-pass path (agg.cu, kernel in agg128.cu)
+bool agg128_native_ok(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, const pac_key_col* keys, int n_keys,
+                      bool masked);
+size_t agg128_native_ws(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap);
+int agg128_native(const int64_t* d_pu_key, const uint64_t* d_mask2, uint64_t salt, const pac_key_col* keys,
+                  int n_keys, const pac_agg_spec* aggs, int n_aggs, int64_t n_rows, const pac_table* out,
+                  int64_t G_cap, void* d_ws, size_t ws_bytes, pac_stream_t stream);
 
 static int grid_for(int64_t work, int per_block, int cap_mult) {
   int dev = 0, sms = 148;
@@ -234,7 +207,8 @@ static int ws128(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, int64_t n_
   off += w->tab_bytes_A;
   w->aggws = off;
   off += w->aggws_bytes;
-  w->bytes = off;
+  // room for the native single-pass path too (whichever path the call takes)
+  w->bytes = std::max(off, agg128_native_ws(aggs, n_aggs, G_cap));
   return PAC_OK;
 }
 
@@ -260,6 +234,9 @@ extern "C" int pac_agg_grouped128(const int64_t* d_pu_key, const uint64_t* d_mas
   if (!d_ws || ws_bytes < w.bytes) return PAC_E_WORKSPACE;
   if (!out->d_num_groups || !out->d_status || !out->d_group_key || !out->d_rows || !out->d_presence)
     return PAC_E_INVAL;
+  if (agg128_native_ok(aggs, n_aggs, G_cap, keys, n_keys, d_mask2 != nullptr))  // one pass, both mask words per row (agg128.cu)
+    return agg128_native(d_pu_key, d_mask2, salt, keys, n_keys, aggs, n_aggs, n_rows, out, G_cap, d_ws, ws_bytes,
+                         stream);
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)d_ws;
   int kinds[PAC_MAX_AGGS] = {0};

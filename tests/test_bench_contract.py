@@ -27,7 +27,7 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "rows/s"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
-    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["config"]["workload"] == "C2"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["config"]["workload"] == "C5"
 
 
 def test_reference_arm_nonzero_rank_is_silent():

@@ -2,7 +2,12 @@
 the 128-bit balanced hash (bit-exact), the 128-world grouped aggregation on BASELINE-shaped
 inputs and on explicit masks with one zero half / both halves zero (bit-exact integers,
 f64 within 1e-9), and finalize over 128 worlds with an m = 128 session (releases per R16,
-posterior 1e-9) over several rounds."""
+posterior 1e-9) over several rounds.  COUNT / SUM / AVG with G_cap <= 32 take the native single-pass
+kernel (k_agg_tiles128): checked against the oracle, against the three-pass path
+(PAC_NO_NATIVE128=1) and at its edges (32 groups, several tiles with a ragged tail, empty input,
+capacity overflow)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -117,3 +122,68 @@ def test_m_mismatch_is_rejected():
     t = ag([None], [], pu_key=to_dev(np.arange(100, dtype=np.int64)), salt=1)
     with pytest.raises(pac.PacError):
         pac.Finalizer(t.kinds, t.G_cap)(s64, t)
+
+
+def _last_kernel(fn):
+    pac.profile_enable(True)
+    try:
+        out = fn()
+        torch.cuda.synchronize()
+        return out, pac.profile_last_kernel()
+    finally:
+        pac.profile_enable(False)
+
+
+@pytest.mark.parametrize("n", [0, 1, 1023, 1025, 333_333])
+def test_native128_explicit_masks_32_groups(orc, n):
+    """the native kernel at its slot limit (32 groups), 2 int64 + 2 f64 columns, zero halves"""
+    rng = np.random.default_rng(n + 17)
+    m = orc.pac_hash128(rng.integers(0, 5000, n).astype(np.int64), 9)
+    if n:
+        m[::5, 0] = 0
+        m[2::9, 1] = 0
+        m[4::17] = 0
+    keys = [rng.integers(0, 32, n).astype(np.int16)]
+    i1 = rng.integers(-(2**40), 2**40, n).astype(np.int64)   # |v| >= 2^26: the GENERIC run body
+    i2 = rng.integers(-100, 100, n).astype(np.int64)
+    f1 = rng.normal(0, 1e3, n)
+    f2 = rng.uniform(0, 1, n)
+    aggs = [(dg.AGG_SUM_I64, i1), (dg.AGG_COUNT, None), (dg.AGG_SUM_I64, i2), (dg.AGG_AVG_F64, f1),
+            (dg.AGG_SUM_F64, f2)]
+    ag = pac.Aggregator128([k for k, _ in aggs], 32)
+    call = lambda: ag(_dev_vals(aggs), [to_dev(keys[0])],  # noqa: E731
+                      mask2=to_dev(np.ascontiguousarray(m).view(np.int64)))
+    t, kern = _last_kernel(call)
+    if n:
+        assert kern.startswith("k_agg_tiles128<2,2>")
+    _cmp(t.to_host(), orc.agg128(m, keys, aggs))
+
+
+@pytest.mark.parametrize("cfg,n,G_cap", [("C2", 2_000_003, 8), ("C1", 70_001, 1)])
+def test_native128_matches_three_pass(cfg, n, G_cap):
+    """same table from the native kernel and from the three 64-world passes (integers bit-exact)"""
+    w = dg.WORKLOADS[cfg]
+    cols = w.host_columns(0, n)
+    aggs = [(k, None if i < 0 else cols["values"][i]) for k, i in w.aggs]
+    ag = pac.Aggregator128([k for k, _ in aggs], G_cap)
+    dv, dk, pu = _dev_vals(aggs), [to_dev(k) for k in cols["keys"]], to_dev(cols["pu"])
+    t1, kern = _last_kernel(lambda: ag(dv, dk, pu_key=pu, salt=77))
+    assert kern.startswith("k_agg_tiles128")
+    a = t1.to_host()
+    os.environ["PAC_NO_NATIVE128"] = "1"
+    try:
+        b = ag(dv, dk, pu_key=pu, salt=77).to_host()
+    finally:
+        del os.environ["PAC_NO_NATIVE128"]
+    _cmp(a, b)
+
+
+def test_native128_capacity_reported():
+    rng = np.random.default_rng(3)
+    n = 50_000
+    keys = rng.integers(0, 9, n).astype(np.int8)
+    ag = pac.Aggregator128([pac.COUNT, pac.SUM_I64], 4)
+    t = ag([None, to_dev(np.ones(n, dtype=np.int64))], [to_dev(keys)],
+           pu_key=to_dev(np.arange(n, dtype=np.int64)), salt=5)
+    torch.cuda.synchronize()
+    assert int(t.status.item()) == pac._lib.PAC_E_CAPACITY
