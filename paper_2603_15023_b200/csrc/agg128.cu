@@ -10,8 +10,9 @@
 //   A2  the 128-bit mask of every row (R28: draw word 0 of pac_hash128; or the caller's [n][2]
 //       masks) and its values, written to the row's slot-sorted position (warp-aggregated cursor
 //       atomics); rows still owing flips queue per warp
-//   A3  the warp finishes its queued masks 32 at a time (pac_hash128_rest: state re-derived from
-//       the partial mask), so a draw word costs one warp pass per 32 rows that need it
+//   A3  the warp finishes its queued masks one draw word per pass (pac_hash128_step on the queued
+//       state), each pass compacting the queue to the rows still owing flips, so a draw word costs
+//       a warp pass per 32 rows that need it rather than per 32 rows
 // Full tiles with 16-byte aligned columns are staged by 1-D TMA bulk copies (p.raw_*), issued
 // when A2 of the previous tile has consumed the buffer, so they land while phase C runs.
 //   C   world-parallel runs: run_body128 -- the transposed Four Russians tables of run_body
@@ -61,7 +62,7 @@ __host__ __device__ constexpr Lay128 lay128(int ni, int nf, int T, int Lcap, int
   L.o_hist = lay_take(off, Lcap * 4);
   L.o_cur = lay_take(off, Lcap * 4);
   L.o_slot = lay_take(off, T);
-  L.o_queue = lay_take(off, 2 * T * 2);  // per-warp queues of rows owing more draw words: pos, row
+  L.o_queue = lay_take(off, T * 8 + 2 * T * 2);  // per-warp queues of rows owing draw words: w, pos, k|maj
   L.o_xcs = lay_take(off, 32 * 16 + 32 * 8);
   L.o_mbar = lay_take(off, 16);
   L.o_misc = lay_take(off, (int)sizeof(Misc));
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(kThreads128, 2) k_agg_tiles128(AggPlan p, Lay1
   uint4* xcs = (uint4*)(smem + L.o_xcs);
   uint2* xcs2 = (uint2*)(smem + L.o_xcs + 32 * 16);
   Misc* misc = (Misc*)(smem + L.o_misc);
-  unsigned short* squeue = (unsigned short*)(smem + L.o_queue);
+  unsigned char* squeue = smem + L.o_queue;
   unsigned long long* mbar = (unsigned long long*)(smem + L.o_mbar);
   unsigned char* raw = smem + L.o_raw;
 
@@ -283,8 +284,9 @@ __global__ void __launch_bounds__(kThreads128, 2) k_agg_tiles128(AggPlan p, Lay1
     const Cols128<decltype(stg)::value, NI, NF> cl{&p, raw, base, T};
     unsigned long long tmax = 0;
     uint32_t emax = 0;
-    unsigned short* qpos = squeue + wid * (T / nw);
-    unsigned short* qrow = squeue + T + wid * (T / nw);
+    unsigned long long* qw = (unsigned long long*)squeue + wid * (T / nw);
+    unsigned short* qpos = (unsigned short*)(squeue + T * 8) + wid * (T / nw);
+    unsigned short* qk = (unsigned short*)(squeue + T * 8) + T + wid * (T / nw);
     int qn = 0;
     for (int li = tid; li < T; li += nth) {
       const int s = sslot[li];
@@ -294,6 +296,9 @@ __global__ void __launch_bounds__(kThreads128, 2) k_agg_tiles128(AggPlan p, Lay1
       b = __shfl_sync(0xffffffffu, b, __ffs(peers) - 1);
       const int pos = b + __popc(peers & lt_mask);
       bool pend = false;
+      uint64_t w = 0;
+      int k = 0;
+      bool maj = false;
       if (s != kNoSlot) {
         uint64_t lo, hi;
         if (masked) {
@@ -301,7 +306,8 @@ __global__ void __launch_bounds__(kThreads128, 2) k_agg_tiles128(AggPlan p, Lay1
           lo = m.x;
           hi = m.y;
         } else {
-          pac_hash128_word0(cl.key(li), p.salt, lo, hi, pend);
+          pac_hash128_word0(cl.key(li), p.salt, lo, hi, w, k, maj);
+          pend = k > 0;
         }
         smask[pos] = lo;
         smask[TS + pos] = hi;
@@ -322,8 +328,9 @@ __global__ void __launch_bounds__(kThreads128, 2) k_agg_tiles128(AggPlan p, Lay1
       const unsigned pm = __ballot_sync(0xffffffffu, pend);
       if (pend) {
         const int q = qn + __popc(pm & lt_mask);
+        qw[q] = w;
         qpos[q] = (unsigned short)pos;
-        qrow[q] = (unsigned short)li;
+        qk[q] = (unsigned short)(k | (maj ? 128 : 0));
       }
       qn += __popc(pm);
     }
@@ -331,12 +338,39 @@ __global__ void __launch_bounds__(kThreads128, 2) k_agg_tiles128(AggPlan p, Lay1
     if (NI > 0 && __any_sync(0xffffffffu, tmax >= (1ull << 26)) && lane == 0) misc->big = 1;
     if (NF > 0 && __any_sync(0xffffffffu, emax == 0x7FF00000u) && lane == 0) misc->nonfinite = 1;
     __syncwarp();
-    for (int qi = lane; qi < qn; qi += 32) {
-      const int pos = qpos[qi];
-      uint64_t lo = smask[pos], hi = smask[TS + pos];
-      pac_hash128_rest(cl.key(qrow[qi]), p.salt, lo, hi);
-      smask[pos] = lo;
-      smask[TS + pos] = hi;
+    // A3: one draw word per pass over the warp's queue, compacted in place to the rows still owing
+    for (int word = 1; qn > 0; ++word) {
+      int nq = 0;
+      for (int qb = 0; qb < qn; qb += 32) {
+        const int qi = qb + lane;
+        bool pend = false;
+        int pos = 0, km = 0;
+        uint64_t w = 0;
+        if (qi < qn) {
+          w = qw[qi];
+          pos = qpos[qi];
+          km = qk[qi];
+          const bool maj = (km & 128) != 0;
+          int k = km & 127;
+          const uint64_t lo = smask[pos], hi = smask[TS + pos];
+          uint64_t c0 = maj ? lo : ~lo, c1 = maj ? hi : ~hi;
+          pac_hash128_step(word, w, c0, c1, k);
+          smask[pos] = maj ? c0 : ~c0;
+          smask[TS + pos] = maj ? c1 : ~c1;
+          pend = k > 0;
+          km = k | (km & 128);
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, pend);  // entries of this pass all read
+        if (pend) {
+          const int q = nq + __popc(pm & lt_mask);  // q <= qi: never an entry not yet read
+          qw[q] = w;
+          qpos[q] = (unsigned short)pos;
+          qk[q] = (unsigned short)km;
+        }
+        nq += __popc(pm);
+      }
+      qn = nq;
+      __syncwarp();
     }
   };
 

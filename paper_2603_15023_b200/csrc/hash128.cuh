@@ -45,43 +45,33 @@ __device__ __forceinline__ void pac_hash128_dev(uint64_t key, uint64_t salt, uin
 }
 
 
-// The same hash in two steps (k_agg_tiles128 finishes the rows that need more than one draw
-// word with full warps, as the 64-world A3 does):
-// word 0: the partial mask after the first 9 draws; pending = flips still owed
+// The same hash as a first draw word plus resumable steps (k_agg_tiles128 finishes the rows that
+// need more than one word in full-warp passes, one word per pass):
+// word 0: the partial mask, and the state to resume from -- w the last draw word, k the flips
+// still owed, maj (the candidates are maj ? mask : ~mask, the majority positions not flipped yet)
 __device__ __forceinline__ void pac_hash128_word0(uint64_t key, uint64_t salt, uint64_t& lo, uint64_t& hi,
-                                                  bool& pending) {
+                                                  uint64_t& w, int& k, bool& maj) {
   const uint64_t x0 = fmix64(key ^ salt);
   const uint64_t x1 = fmix64(x0 ^ kHi128);
   const int c = __popcll(x0) + __popcll(x1);
-  const bool maj = c > 64;
-  int k = maj ? c - 64 : 64 - c;
+  maj = c > 64;
+  k = maj ? c - 64 : 64 - c;
   uint64_t c0 = maj ? x0 : ~x0, c1 = maj ? x1 : ~x1;
-  draw_word128(fmix64(x0 ^ x1 ^ kDrawSeed), c0, c1, k);
+  w = fmix64(x0 ^ x1 ^ kDrawSeed);
+  draw_word128(w, c0, c1, k);
   lo = maj ? c0 : ~c0;
   hi = maj ? c1 : ~c1;
-  pending = k > 0;
 }
-// words 1.. from the partial mask: the candidates are the majority positions not flipped yet
-// (c = maj ? mask : ~mask) and the flips still owed are |c - 64| minus the bits already flipped
-__device__ __forceinline__ void pac_hash128_rest(uint64_t key, uint64_t salt, uint64_t& lo, uint64_t& hi) {
-  const uint64_t x0 = fmix64(key ^ salt);
-  const uint64_t x1 = fmix64(x0 ^ kHi128);
-  const int c = __popcll(x0) + __popcll(x1);
-  const bool maj = c > 64;
-  int k = (maj ? c - 64 : 64 - c) - __popcll(x0 ^ lo) - __popcll(x1 ^ hi);
-  uint64_t c0 = maj ? lo : ~lo, c1 = maj ? hi : ~hi;
-  uint64_t w = fmix64(x0 ^ x1 ^ kDrawSeed);
-#pragma unroll 1
-  for (int word = 1; word < 64 && k > 0; ++word) {
-    w = fmix64(w + kDrawStep);
-    draw_word128(w, c0, c1, k);
+// draw word `word` (1..63) on a resumed state; after word 63 the safety net of pac_hash128_dev
+__device__ __forceinline__ void pac_hash128_step(int word, uint64_t& w, uint64_t& c0, uint64_t& c1, int& k) {
+  w = fmix64(w + kDrawStep);
+  draw_word128(w, c0, c1, k);
+  if (word == 63) {
+    while (k > 0) {
+      if (c0) c0 &= c0 - 1; else c1 &= c1 - 1;
+      --k;
+    }
   }
-  while (k > 0) {
-    if (c0) c0 &= c0 - 1; else c1 &= c1 - 1;
-    --k;
-  }
-  lo = maj ? c0 : ~c0;
-  hi = maj ? c1 : ~c1;
 }
 
 }  // namespace pac
