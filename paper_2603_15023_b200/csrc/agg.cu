@@ -1392,6 +1392,41 @@ void profile_end(cudaStream_t st);
 
 using namespace pac;
 
+namespace pac {
+// ------------------------------------------------------------------ partition-first (part.cu)
+constexpr int kPartCols = 2 + PAC_MAX_KEYS + 5;
+struct PartResult {
+  const void* col[kPartCols];
+  const longlong2* units;
+  const int* n_units;
+  int* unit_ctr;
+  int64_t rows;
+};
+size_t part_ws_bytes(int64_t n_rows, int n_cols_max, int row_bytes, int pbits, int grid, int unit_rows);
+int part_rows(const void* const* src, const int* eb, int ncol, int hash0, uint64_t salt, int n_keys,
+              int64_t n_rows, int pbits, int grid, int unit_rows, char* ws, PartResult* out, cudaStream_t st);
+constexpr int kPartUnitRows = 32768;    // rows per unit (a multiple of the tile rows)
+constexpr int64_t kPartMinRows = 1 << 20;
+
+// Partition-first (opt-in, PAC_PART=1: measured slower than the deferred tier on C3)
+// applies to large inputs whose table has many more groups than the TMEM CTA table holds
+// (G_cap >= 4 Lcap); P = 2^pbits partitions of <= Lcap / 2 groups by capacity.
+static bool want_partition(int64_t G_cap, int64_t n_rows, const SmemLayout& L, int* pbits) {
+  if (!getenv("PAC_PART") || !L.tm || G_cap < 4 * (int64_t)L.Lcap || n_rows < kPartMinRows) return false;
+  int b = 7;
+  while (b < 15 && ((int64_t)1 << b) * (L.Lcap / 2) < G_cap) ++b;
+  if (n_rows + (16ll << b) >= INT32_MAX) return false;
+  *pbits = b;
+  return true;
+}
+static int part_grid(int sms) { return 2 * sms; }
+// worst-case bytes per row of the partitioned columns: mask/pu 8, keys <= 8, values 8 each
+static size_t part_ws_for(const AccSet& A, int64_t n_rows, int pbits, int sms) {
+  const int nv = A.ni + A.nf + ((A.has_min || A.has_max) ? 1 : 0);
+  return part_ws_bytes(n_rows, 1 + PAC_MAX_KEYS + nv, 16 + 8 * nv, pbits, part_grid(sms), kPartUnitRows);
+}
+}  // namespace pac
+
 extern "C" int pac_mask(const int64_t* d_pu_key, int64_t n, uint64_t salt, uint64_t* d_mask,
                         pac_stream_t stream) {
   if (n < 0 || (n > 0 && (!d_pu_key || !d_mask))) return PAC_E_INVAL;
@@ -1431,6 +1466,8 @@ extern "C" int pac_agg_workspace_size_rows(const pac_agg_spec* aggs, int n_aggs,
   if (!choose_layout(A, G_cap, smem_max, 8, &L)) return PAC_E_INVAL;
   if (G_cap <= L.Lcap) return PAC_OK;  // every group can hold a CTA-local slot: no tier rows
   *bytes = spill_layout(A, G_cap, base, std::min<int64_t>(spill_rows_needed(n_rows), INT32_MAX - 1)).bytes + 4 * 256;
+  int pbits = 0;
+  if (want_partition(G_cap, n_rows, L, &pbits)) *bytes = std::max(*bytes, base + part_ws_for(A, n_rows, pbits, sms));
   return PAC_OK;
 }
 
@@ -1594,6 +1631,50 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
     } else {
       SmemLayout L{};
       if (!choose_layout(A, G_cap, smem_max, width, &L)) return PAC_E_INVAL;
+      // partition-first (part.cu): the rows reordered by group hash into the workspace, the
+      // TMEM kernel then runs unit by unit over them (masks in, no hashing, no deferred tier)
+      int pbits = 0;
+      bool part = want_partition(G_cap, n_rows, L, &pbits) && ws_bytes >= W.bytes + part_ws_for(A, n_rows, pbits, sms);
+      if (part) {
+        const void* src[kPartCols];
+        int eb[kPartCols];
+        int nc = 0;
+        src[nc] = d_mask ? (const void*)d_mask : (const void*)d_pu_key;
+        eb[nc++] = 8;
+        for (int c = 0; c < n_keys; ++c) {
+          src[nc] = keys[c].d_col;
+          eb[nc++] = keys[c].elem_bytes;
+        }
+        for (int c = 0; c < A.ni; ++c) {
+          src[nc] = A.icol[c];
+          eb[nc++] = 8;
+        }
+        for (int c = 0; c < A.nf; ++c) {
+          src[nc] = A.fcol[c];
+          eb[nc++] = 8;
+        }
+        if (A.has_min || A.has_max) {
+          src[nc] = A.mcol;
+          eb[nc++] = 8;
+        }
+        PartResult pr{};
+        profile_begin(st, "k_part_{hist,totals,scan,offsets,scatter} x2");
+        int prc = part_rows(src, eb, nc, d_pu_key ? 1 : 0, salt, n_keys, n_rows, pbits, part_grid(sms), kPartUnitRows,
+                            ws + W.bytes, &pr, st);
+        profile_end(st);
+        if (prc != PAC_OK) return prc;
+        int k = 0;
+        p.pu_key = nullptr;
+        p.mask_in = (const unsigned long long*)pr.col[k++];
+        for (int c = 0; c < n_keys; ++c) p.key_col[c] = pr.col[k++];
+        for (int c = 0; c < A.ni; ++c) p.icol[c] = (const long long*)pr.col[k++];
+        for (int c = 0; c < A.nf; ++c) p.fcol[c] = (const double*)pr.col[k++];
+        if (A.has_min || A.has_max) p.mcol = (const double*)pr.col[k++];
+        p.n_rows = pr.rows;
+        p.units = pr.units;
+        p.n_units = pr.n_units;
+        p.unit_ctr = pr.unit_ctr;
+      }
       // raw columns staged per tile by TMA (k_agg_tiles reads them from smem)
       {
         int off = 0;
@@ -1607,11 +1688,11 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
           ++p.nraw;
         };
         p.nraw = 0;
-        add(d_mask ? (const void*)d_mask : (const void*)d_pu_key, 8);
-        for (int c = 0; c < A.ni; ++c) add(A.icol[c], 8);
-        for (int c = 0; c < A.nf; ++c) add(A.fcol[c], 8);
-        if (A.has_min || A.has_max) add(A.mcol, 8);
-        for (int c = 0; c < n_keys; ++c) add(keys[c].d_col, keys[c].elem_bytes);
+        add(p.mask_in ? (const void*)p.mask_in : (const void*)p.pu_key, 8);
+        for (int c = 0; c < A.ni; ++c) add(p.icol[c], 8);
+        for (int c = 0; c < A.nf; ++c) add(p.fcol[c], 8);
+        if (A.has_min || A.has_max) add(p.mcol, 8);
+        for (int c = 0; c < n_keys; ++c) add(p.key_col[c], keys[c].elem_bytes);
         int copied = 0;
         for (int i = 0; i < p.nraw; ++i) copied += L.T * p.raw_eb[i];
         p.raw_bytes = copied;
@@ -1627,7 +1708,7 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
       const int mm = (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0);
       // deferred HBM tier when groups can miss a CTA-local slot and the workspace has room
       SpillLayout S{};
-      if (G_cap > L.Lcap && !getenv("PAC_NO_SPILL")) {
+      if (G_cap > L.Lcap && !part && !getenv("PAC_NO_SPILL")) {
         const int64_t cap = spill_fit(A, G_cap, W.bytes, ws_bytes, n_rows);
         if (cap > 0) S = spill_layout(A, G_cap, W.bytes, cap);
       }
@@ -1643,7 +1724,7 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
       }
       char kname[96];
       snprintf(kname, sizeof(kname), "%s<%d,%d,%d>%s", L.tm ? "k_agg_tiles_tm" : "k_agg_tiles", A.ni, A.nf, mm,
-               S.cap > 0 ? " + k_spill_{resolve,offsets,scatter,agg}" : "");
+               S.cap > 0 ? " + k_spill_{resolve,offsets,scatter,agg}" : (part ? " (partition units)" : ""));
       profile_begin(st, kname);  // the timed region covers the whole aggregation pass
       e = L.tm ? kLaunchTm[A.ni][A.nf][mm](p, L, sms, st) : kLaunch[A.ni][A.nf][mm](p, L, sms, st);
       if (e == cudaSuccess && S.cap > 0) {

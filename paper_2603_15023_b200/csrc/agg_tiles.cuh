@@ -77,6 +77,11 @@ struct AggPlan {
   unsigned long long* sp_val;
   int* sp_cnt;  // [G_cap] records per provisional slot
   int m128;     // 1: provisional world rows are 128 words (k_agg_tiles128, agg128.cu)
+  // partition-first input (part.cu): the CTA takes row ranges [x, y) from `units` through the
+  // global counter unit_ctr and flushes and resets its table after each (k_agg_tiles_tm)
+  const longlong2* units;
+  const int* n_units;
+  int* unit_ctr;
 };
 
 struct SmemLayout {

@@ -228,71 +228,115 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_agg_tiles_tm(AggPlan p, SmemL
 
   const int64_t ntiles = (p.n_rows + T - 1) / T;
   const int64_t t_per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const int64_t t0 = (int64_t)blockIdx.x * t_per;
-  const int64_t t1 = min(ntiles, t0 + t_per);
-  auto staged_tile = [&](int64_t t) { return p.tma_ok && t < t1 && (t + 1) * T <= p.n_rows; };
-  auto tile_rows = [&](int64_t t) { return (int)min((int64_t)T, p.n_rows - t * T); };
+  __shared__ long long s_unit[2];
   uint32_t phase = 0;
-  if (tid == 0) {
-    mbar_init(mbar, 1);
-    if (staged_tile(t0)) issue_tile(p, raw, mbar, t0 * T, T);
-  }
+  if (tid == 0) mbar_init(mbar, 1);
   __syncthreads();
 
   SpillCur sc;
   sc.init();
-  if (t0 < t1) {
-    if (staged_tile(t0)) {
-      mbar_wait(mbar, phase);
-      phase ^= 1u;
-      tile_a1<NI, NF, MM, true>(p, sm, L, t0 * T, tile_rows(t0), sc);
-    } else {
-      tile_a1<NI, NF, MM, false>(p, sm, L, t0 * T, tile_rows(t0), sc);
-    }
-  }
-  for (int64_t tile = t0; tile < t1; ++tile) {
-    const int64_t base = tile * T;
-    const bool staged = staged_tile(tile);
-    __syncthreads();  // A1(tile) and C(tile-1) complete
-    if (staged) tile_mid<NI, NF, MM, true>(p, sm, L, base, maxabs);
-    else tile_mid<NI, NF, MM, false>(p, sm, L, base, maxabs);
-    const bool next_staged = staged_tile(tile + 1);
-    if (tid == 0 && next_staged) issue_tile(p, raw, mbar, (tile + 1) * T, T);
-
-    // ---------------- C: each owner warp runs the runs of its slots, then adds them to TMEM
-    {
-      const bool small = (NI == 0) || misc->big == 0;
-      const bool fin = (NF == 0) || misc->nonfinite == 0;
-      const XposeConst xc = load_xpose(sm.xcs, sm.xcs2, lane);
-      for (int k = 0; k < K; ++k) {
-        const int s = q + 4 * oi + 16 * k;
-        if (s >= Lcap) break;
-        const int rb = sm.runoffs[s], re = sm.runoffs[s + 1];
-        if (rb == re) continue;
-        WarpAcc<NI, NF, MM> acc;
-        acc.cur = s;
-        acc.reset();
-        for (int r = rb; r < re; ++r) {
-          const uint32_t d = sm.rdesc[r];
-          const int beg = (int)(d & 0xFFFFu);
-          const int len = (int)(d >> 26) + 1;
-          if (small && fin)
-            run_body<NI, NF, MM, false>(acc, sm.smask + beg, sm.sival + beg, L.TS, sm.sfval + beg, L.TS,
-                                        sm.smval + beg, len, xc, lane);
-          else
-            run_body<NI, NF, MM, true>(acc, sm.smask + beg, sm.sival + beg, L.TS, sm.sfval + beg, L.TS,
-                                       sm.smval + beg, len, xc, lane, small, fin);
-        }
-        tm_flush<NI, NF, MM>(acc, tm_slot_addr(tbase, s, K, S::wps));
+  // Row ranges: without units, the CTA's contiguous share of the tiles; with units (partitioned
+  // input), units taken from the global counter, the CTA table flushed and reset after each.
+  for (int it = 0;; ++it) {
+    int64_t r0, r1;
+    if (p.units) {
+      if (tid == 0) {
+        const int u = atomicAdd(p.unit_ctr, 1);
+        const bool ok = u < *p.n_units;
+        s_unit[0] = ok ? p.units[u].x : 0;
+        s_unit[1] = ok ? p.units[u].y : -1;
       }
+      __syncthreads();
+      r0 = s_unit[0];
+      r1 = s_unit[1];
+      if (r1 < 0) break;
+    } else {
+      if (it > 0) break;
+      const int64_t t0 = (int64_t)blockIdx.x * t_per;
+      r0 = t0 * T;
+      r1 = min(p.n_rows, (t0 + t_per) * T);
     }
-    if (tile + 1 < t1) {
-      if (next_staged) {
+    const int64_t nt = r1 > r0 ? (r1 - r0 + T - 1) / T : 0;
+    auto staged_tile = [&](int64_t i) { return p.tma_ok && i < nt && r0 + (i + 1) * T <= r1; };
+    auto tile_rows = [&](int64_t i) { return (int)min((int64_t)T, r1 - (r0 + i * T)); };
+    if (tid == 0 && staged_tile(0)) issue_tile(p, raw, mbar, r0, T);
+    if (nt > 0) {
+      if (staged_tile(0)) {
         mbar_wait(mbar, phase);
         phase ^= 1u;
-        tile_a1<NI, NF, MM, true>(p, sm, L, base + T, tile_rows(tile + 1), sc);
+        tile_a1<NI, NF, MM, true>(p, sm, L, r0, T, sc);
       } else {
-        tile_a1<NI, NF, MM, false>(p, sm, L, base + T, tile_rows(tile + 1), sc);
+        tile_a1<NI, NF, MM, false>(p, sm, L, r0, tile_rows(0), sc);
+      }
+    }
+    for (int64_t i = 0; i < nt; ++i) {
+      const int64_t base = r0 + i * T;
+      const bool staged = staged_tile(i);
+      __syncthreads();  // A1(tile) and C(tile-1) complete
+      if (staged) tile_mid<NI, NF, MM, true>(p, sm, L, base, maxabs);
+      else tile_mid<NI, NF, MM, false>(p, sm, L, base, maxabs);
+      const bool next_staged = staged_tile(i + 1);
+      if (tid == 0 && next_staged) issue_tile(p, raw, mbar, base + T, T);
+
+      // ---------------- C: each owner warp runs the runs of its slots, then adds them to TMEM
+      {
+        const bool small = (NI == 0) || misc->big == 0;
+        const bool fin = (NF == 0) || misc->nonfinite == 0;
+        const XposeConst xc = load_xpose(sm.xcs, sm.xcs2, lane);
+        for (int k = 0; k < K; ++k) {
+          const int s = q + 4 * oi + 16 * k;
+          if (s >= Lcap) break;
+          const int rb = sm.runoffs[s], re = sm.runoffs[s + 1];
+          if (rb == re) continue;
+          WarpAcc<NI, NF, MM> acc;
+          acc.cur = s;
+          acc.reset();
+          for (int r = rb; r < re; ++r) {
+            const uint32_t d = sm.rdesc[r];
+            const int beg = (int)(d & 0xFFFFu);
+            const int len = (int)(d >> 26) + 1;
+            if (small && fin)
+              run_body<NI, NF, MM, false>(acc, sm.smask + beg, sm.sival + beg, L.TS, sm.sfval + beg, L.TS,
+                                          sm.smval + beg, len, xc, lane);
+            else
+              run_body<NI, NF, MM, true>(acc, sm.smask + beg, sm.sival + beg, L.TS, sm.sfval + beg, L.TS,
+                                         sm.smval + beg, len, xc, lane, small, fin);
+          }
+          tm_flush<NI, NF, MM>(acc, tm_slot_addr(tbase, s, K, S::wps));
+        }
+      }
+      if (i + 1 < nt) {
+        if (next_staged) {
+          mbar_wait(mbar, phase);
+          phase ^= 1u;
+          tile_a1<NI, NF, MM, true>(p, sm, L, base + T, T, sc);
+        } else {
+          tile_a1<NI, NF, MM, false>(p, sm, L, base + T, tile_rows(i + 1), sc);
+        }
+      }
+    }
+    if (p.units) {
+      // ---------------- end of a unit: its slots to the provisional HBM table, then a fresh table
+      __syncthreads();
+      const int nl = min(misc->nlocal, Lcap);
+      for (int k = 0; k < K; ++k) {
+        const int s = q + 4 * oi + 16 * k;
+        if (s >= nl) break;
+        const uint32_t a = tm_slot_addr(tbase, s, K, S::wps);
+        tm_to_hbm<NI, NF, MM>(p, a, sm.lprov[s], lane);
+        tm_init_slot<NI, NF, MM>(a);
+      }
+      tm_wait_st();
+      for (int s = tid; s < nl; s += nth) {
+        if (sm.lprov[s] >= 0 && sm.lrows[s]) atomicAdd(&p.prov_rows[sm.lprov[s]], sm.lrows[s]);
+        sm.lrows[s] = 0;
+      }
+      for (int i = tid; i < LH; i += nth) sm.lstate[i] = 0;
+      __syncthreads();  // every thread has read nlocal
+      if (tid == 0) {
+        atomicMax(&p.dbg[1], (unsigned long long)misc->nlocal);
+        misc->nlocal = 0;
+        misc->ndict = 0;
       }
     }
   }
