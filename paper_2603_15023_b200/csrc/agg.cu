@@ -21,6 +21,7 @@
 #include "agg_tiles.cuh"
 #include "agg_tm.cuh"
 #include "agg_ws.cuh"
+#include "agg_lean.cuh"
 
 namespace pac {
 
@@ -269,12 +270,7 @@ __device__ __forceinline__ void mmv_refresh(const AggPlan& p, int pv, int s, dou
 // CTA dictionary for one int32 key column: entry = (code << 32) | packed key in one 64-bit word
 // (0 = empty; code 0xFFFFFFFF = being written), so a lookup is one shared load and one compare.
 // Codes as local_code's: s + 1 for local slot s, kOvfBase + HBM slot + 1 for a key with none.
-__device__ __forceinline__ unsigned long long ld_acquire_cta_shared_u64(const unsigned long long* a) {
-  unsigned long long v;
-  asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"((uint32_t)__cvta_generic_to_shared(a))
-               : "memory");
-  return v;
-}
+// (ld_acquire_cta_shared_u64: agg_lean.cuh)
 static __device__ int local_code32(const AggPlan& p, uint32_t key, unsigned long long* dent, int LH, int* lprov,
                                    int Lcap, Misc* misc, double* bmin, double* bmax) {
   uint32_t h = (key * 0x9E3779B1u) >> 16 & (LH - 1);
@@ -1627,6 +1623,12 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
       snprintf(kname, sizeof(kname), "k_agg_ws<%d,%d,0>", A.ni, A.nf);
       profile_begin(st, kname);
       e = kLaunchWs[A.ni][A.nf](p, WL, sms, st);
+      profile_end(st);
+    } else if (lean_applicable(A.ni, A.nf, A.has_min, A.has_max, A.has_count, n_keys, width, G_cap,
+                               d_pu_key != nullptr)) {
+      // every group fits a CTA-local slot and the key packs into 4 bytes: k_agg_lean (agg_lean.cuh)
+      char kname[64];
+      e = launch_lean(p, n_keys, width, sms, st, kname, (int)sizeof(kname));  // opens the profile region
       profile_end(st);
     } else {
       SmemLayout L{};
