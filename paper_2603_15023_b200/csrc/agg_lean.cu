@@ -5,7 +5,7 @@
 namespace pac {
 
 typedef void (*LeanKernel)(AggPlan, int, int);
-template <int KS> LeanKernel lean_kernel(int ni, int nf);  // agg_lean_ks*.cu
+template <int KS, int OWN> LeanKernel lean_kernel(int ni, int nf);  // agg_lean_ks*.cu
 void profile_begin(cudaStream_t st, const char* name);  // runtime.cu
 
 bool lean_applicable(int ni, int nf, int has_min, int has_max, int has_count, int n_keys, int key_width,
@@ -45,13 +45,15 @@ cudaError_t launch_lean(AggPlan& p, int n_keys, int key_width, int sms, cudaStre
   for (int i = 0; i < p.nraw; ++i) copied += kLeanT * p.raw_eb[i];
   p.raw_bytes = copied;
   p.tma_ok = (aligned && !getenv("PAC_NO_TMA")) ? 1 : 0;
-  LeanKernel k = KS == 0 ? lean_kernel<0>(ni, nf) : KS == 1 ? lean_kernel<1>(ni, nf) : lean_kernel<2>(ni, nf);
+  LeanKernel k = KS == 0 ? lean_kernel<0, 0>(ni, nf)
+                 : KS == 1 ? (owner ? lean_kernel<1, 1>(ni, nf) : lean_kernel<1, 0>(ni, nf))
+                           : (owner ? lean_kernel<2, 1>(ni, nf) : lean_kernel<2, 0>(ni, nf));
   if (!k) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (p.n_rows + kLeanT - 1) / kLeanT;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms));
-  snprintf(kname, kname_len, "k_agg_lean<%d,%d,%d>", ni, nf, KS);
+  snprintf(kname, kname_len, "k_agg_lean<%d,%d,%d,%d>", ni, nf, KS, owner ? 1 : 0);
   if (getenv("PAC_DEBUG"))
     fprintf(stderr, "[libpac] %s %d CTAs x %d threads, mode %s, lcap %d, smem %d B, tma %d\n", kname, grid,
             kLeanThreads, owner ? "owner" : "private", lcap, L.bytes, p.tma_ok);

@@ -20,6 +20,16 @@
 
 namespace pac {
 
+#ifndef PAC_LEAN_CSFLAT
+#define PAC_LEAN_CSFLAT 0  // 1: the carry-slot map written lane-parallel after phase B
+#endif
+#ifndef PAC_LEAN_QBAL
+#define PAC_LEAN_QBAL 0  // (measured slower on C5: 45.8 vs 44.6 ms) owner mode: slot s in TMEM quarter s % 4, its quarter's 4 warps split the slots by runs
+#endif
+#ifndef PAC_LEAN_WORKLIST
+#define PAC_LEAN_WORKLIST 0  // 1: owner warps iterate a ballot-built list of their slots with runs
+#endif
+
 constexpr int kLeanT = 2048;      // rows per tile
 constexpr int kLeanLcap = 128;    // local slots
 constexpr int kLeanLH = 256;      // dictionary entries (2 x Lcap)
@@ -158,8 +168,14 @@ __device__ __forceinline__ uint32_t lean_key(const AggPlan& p, const unsigned ch
 
 // TMEM column of slot s for warp w: mode P = w's private copy; mode O = s's owner (w == s % 16)
 __device__ __forceinline__ uint32_t lean_taddr(uint32_t tbase, int w, int s, int wps, bool owner) {
+  if (PAC_LEAN_QBAL && owner)  // quarter s % 4, any of its 4 warps (one per slot and tile)
+    return tbase + ((uint32_t)(32 * (s & 3)) << 16) + (uint32_t)((s >> 2) * wps);
   const int col = (w >> 2) * 128 + (owner ? (s >> 4) : s) * wps;
   return tbase + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)col;
+}
+// owner mode: the slots warp w initialises / drains (fixed; mode O's per-tile split is dynamic)
+__device__ __forceinline__ bool lean_mine(int w, int s) {
+  return PAC_LEAN_QBAL ? ((s & 3) == (w & 3) && ((s >> 2) & 3) == (w >> 2)) : ((s & 15) == w);
 }
 
 
@@ -200,7 +216,9 @@ struct LeanB {
   int cc[4], co[4];  // rows carried into the current tile and their carry-area offsets (slot order)
 };
 
-template <int NI, int NF, int KS>
+// OWN: 1 = mode O (slot owners), 0 = mode P (private copies) -- separate instances, so each mode
+// gets its own register allocation
+template <int NI, int NF, int KS, int OWN>
 __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int owner_mode, int lcap) {
   constexpr LeanLayout L = lean_layout(NI, NF);
   constexpr int T = kLeanT, TS = L.TS, CC = L.CC, Lcap = kLeanLcap, NW = kLeanNW, RPT = T / kLeanThreads;
@@ -236,7 +254,8 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
   const int tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const bool owner = owner_mode != 0;
+  constexpr bool owner = OWN != 0;
+  (void)owner_mode;
   // this warp's private phase-B results: wpv[s] = sorted base of s's new rows | copy-in offset << 16
   uint32_t* wpv = (uint32_t*)(smem + L.o_wpv) + wid * Lcap;
 
@@ -269,7 +288,7 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
   }
   // zero this warp's table columns: mode P its private copy of every slot, mode O its own slots
   for (int s = 0; s < lcap; ++s) {
-    if (owner && (s & 15) != wid) continue;
+    if (owner && !lean_mine(wid, s)) continue;
     tm_init_slot<NI, NF, 0>(lean_taddr(tbase, wid, s, S::wps, owner));
   }
   tm_wait_st();
@@ -339,6 +358,7 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
     // new rows), region offsets (even rows: run_body reads 16-byte row pairs), full runs, the
     // leftovers' places in the carry area.  Warp 0 publishes what phase C needs.
     int nruns, ncarry_out;
+    unsigned owned_work;  // bit q: owned slot wid + 16 q has runs this tile (mode O)
     {
       const int4 h4 = *(const int4*)(hp + 4 * lane);
       const int n[4] = {h4.x, h4.y, h4.z, h4.w};
@@ -375,6 +395,8 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
       ncarry_out = min((int)(all >> 16), CC);
       LeanB nb;
       uint32_t wv[4];
+      int my_oy = 0, my_valid = 0, my_l4 = 0, my_runs = 0;
+      bool my_work = false;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int s = 4 * lane + k;
@@ -388,17 +410,23 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
           scpo[s] = ox + (tot[k] & ~31) - oy;
           lrows[s] += (unsigned long long)n[k];
         }
-        // owner warp of s (s % 16; k == wid % 4 is warp-uniform): its carry-slot map entries, 4 per
-        // store, and (private mode) run descriptors
-        if (k == (wid & 3) && (lane & 3) == (wid >> 2)) {
-          const int valid = fl ? 0 : l[k];
-          const uint32_t s4 = (uint32_t)s * 0x01010101u;
-          for (int i = 0; i < l2[k] && oy + i < CC; i += 4) {
-            const int m = min(max(valid - i, 0), 4);
-            const uint32_t keep = m == 4 ? 0xFFFFFFFFu : ((1u << (8 * m)) - 1u);
-            *(uint32_t*)(cs_out + oy + i) = (s4 & keep) | ~keep;
+        // the slots of this warp's lane column (s % 16 == wid for the lanes with L % 4 == wid / 4;
+        // k == wid % 4 is warp-uniform): carry range, work flag, run descriptors (private mode)
+        if (k == (wid & 3)) {
+          my_oy = oy;
+          my_valid = fl ? 0 : l[k];
+          my_l4 = l2[k];
+          my_work = tot[k] >= 32 || fl;
+          my_runs = f[k] + ((fl && l[k]) ? 1 : 0);
+          if (!PAC_LEAN_CSFLAT && (lane & 3) == (wid >> 2)) {
+            const uint32_t s4 = (uint32_t)s * 0x01010101u;
+            for (int i = 0; i < l2[k] && oy + i < CC; i += 4) {
+              const int m = min(max(my_valid - i, 0), 4);
+              const uint32_t keep = m == 4 ? 0xFFFFFFFFu : ((1u << (8 * m)) - 1u);
+              *(uint32_t*)(cs_out + oy + i) = (s4 & keep) | ~keep;
+            }
           }
-          if (!owner)
+          if (!owner && (lane & 3) == (wid >> 2))
             for (int i = 0; i < f[k]; ++i) rdesc[oz + i] = pack_run(ox + 32 * i, s, 32);
         }
         nb.cc[k] = fl ? 0 : l[k];
@@ -408,6 +436,39 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
         oz += f[k];
       }
       *(uint4*)(wpv + 4 * lane) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      // owned slots s = wid + 16 q (q < 8) live in lane (wid / 4) + 4 q: their carry-slot map
+      // entries, 4 per store, lane j: slot q = j / 8 (+ 4 in the second pass), word j % 8
+      const int col = wid >> 2;
+#pragma unroll
+      for (int pass = 0; pass < (PAC_LEAN_CSFLAT ? 2 : 0); ++pass) {
+        const int q = (lane >> 3) + 4 * pass, e = lane & 7, src = col + 4 * q;
+        const int qy = __shfl_sync(0xffffffffu, my_oy, src);
+        const int qv = __shfl_sync(0xffffffffu, my_valid, src);
+        const int ql = __shfl_sync(0xffffffffu, my_l4, src);
+        if (4 * e < ql && qy + 4 * e < CC) {
+          const int m = min(max(qv - 4 * e, 0), 4);
+          const uint32_t keep = m == 4 ? 0xFFFFFFFFu : ((1u << (8 * m)) - 1u);
+          *(uint32_t*)(cs_out + qy + 4 * e) = (((uint32_t)(wid + 16 * q) * 0x01010101u) & keep) | ~keep;
+        }
+      }
+      owned_work = 0;
+      if (PAC_LEAN_QBAL && owner) {
+        // quarter q = wid % 4 holds slots 4 L + q (this lane's my_*); its 4 warps take contiguous
+        // lane ranges of about equal run counts, warp wid / 4 the ((wid / 4))-th
+        int incl = my_runs;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int a = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += a;
+        }
+        const int W = max(__shfl_sync(0xffffffffu, incl, 31), 1);
+        const int chunk = min(3, (4 * (incl - my_runs) + 2 * my_runs) / W);  // by the run midpoint
+        owned_work = __ballot_sync(0xffffffffu, my_work && chunk == (wid >> 2));
+      } else if (PAC_LEAN_WORKLIST) {
+        const unsigned wb = __ballot_sync(0xffffffffu, my_work);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) owned_work |= ((wb >> (col + 4 * q)) & 1u) << q;
+      }
       __syncwarp();
       // A2's copy-in reads the offsets of the rows carried INTO this tile (cb.co, set above);
       // the next tile carries nb
@@ -515,11 +576,41 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
       const int fl = *gflag;
       const bool small = (NI == 0) || !(fl & 1);
       const bool fin = (NF == 0) || !(fl & 2);
-      if (owner) {
+      if (owner && PAC_LEAN_QBAL) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");  // slots change warps between tiles
+        for (unsigned wk = owned_work; wk; wk &= wk - 1) {
+          const int s = 4 * (__ffs(wk) - 1) + (wid & 3);
+          const int tot = stot[s];
+          const int lf = slfl[s];
+          const int o = soff[s], f = tot >> 5;
+          for (int i = 0; i < f; ++i) {
+            const int b = o + 32 * i;
+            if (small && fin)
+              run_body<NI, NF, 0, false>(acc, smask + b, sival + b, TS, sfval + b, TS, nullptr, 32, xc, lane);
+            else
+              run_body<NI, NF, 0, true>(acc, smask + b, sival + b, TS, sfval + b, TS, nullptr, 32, xc, lane, small,
+                                        fin);
+          }
+          const int l = tot & 31;
+          if (l && lf)
+            run_body<NI, NF, 0, true>(acc, smask + o + 32 * f, sival + o + 32 * f, TS, sfval + o + 32 * f, TS, nullptr,
+                                      l, xc, lane, small, false);
+          tm_flush<NI, NF, 0>(acc, lean_taddr(tbase, wid, s, S::wps, true));
+          acc.reset();
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      } else if (owner) {
+#if PAC_LEAN_WORKLIST
+        for (unsigned wk = owned_work; wk; wk &= wk - 1) {
+          const int s = wid + 16 * (__ffs(wk) - 1);
+          const int tot = stot[s];
+          const int lf = slfl[s];
+#else
         for (int s = wid; s < Lcap; s += NW) {
           const int tot = stot[s];
           const int lf = slfl[s];
           if (tot < 32 && !lf) continue;  // nothing to run: the rows wait in the carry area
+#endif
           const int o = soff[s], f = tot >> 5;
           for (int i = 0; i < f; ++i) {
             const int b = o + 32 * i;
@@ -587,6 +678,7 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
 
   // ---------------- the rows still in the carry area: one partial run per slot (owner / s % 16)
   for (int s = wid; s < Lcap; s += NW) {
+    if (PAC_LEAN_QBAL && owner && !lean_mine(wid, s)) continue;
     const int src = (s >> 2), k = s & 3;
     const int c0 = __shfl_sync(0xffffffffu, k == 0 ? cb.cc[0] : k == 1 ? cb.cc[1] : k == 2 ? cb.cc[2] : cb.cc[3], src);
     const int o0 = __shfl_sync(0xffffffffu, k == 0 ? cb.co[0] : k == 1 ? cb.co[1] : k == 2 ? cb.co[2] : cb.co[3], src);
@@ -603,7 +695,7 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
   // ---------------- TMEM -> provisional HBM table, rows, the overflow bound
   const int nloc = min(misc->nlocal, lcap);
   for (int s = 0; s < nloc; ++s) {
-    if (owner && (s & 15) != wid) continue;
+    if (owner && !lean_mine(wid, s)) continue;
     tm_to_hbm<NI, NF, 0>(p, lean_taddr(tbase, wid, s, S::wps, owner), lprov[s], lane);
   }
   for (int s = tid; s < nloc; s += kLeanThreads)

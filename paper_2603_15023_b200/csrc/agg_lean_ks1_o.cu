@@ -1,0 +1,21 @@
+// libpac: k_agg_lean instances for key spec KS = 1, mode O (slot owners) (agg_lean.cuh)
+#include "agg_lean.cuh"
+
+namespace pac {
+typedef void (*LeanKernel)(AggPlan, int, int);
+template <int KS, int OWN> LeanKernel lean_kernel(int ni, int nf);
+template <>
+LeanKernel lean_kernel<1, 1>(int ni, int nf) {
+  switch (ni * 3 + nf) {
+    case 0: return k_agg_lean<0, 0, 1, 1>;
+    case 1: return k_agg_lean<0, 1, 1, 1>;
+    case 2: return k_agg_lean<0, 2, 1, 1>;
+    case 3: return k_agg_lean<1, 0, 1, 1>;
+    case 4: return k_agg_lean<1, 1, 1, 1>;
+    case 5: return k_agg_lean<1, 2, 1, 1>;
+    case 6: return k_agg_lean<2, 0, 1, 1>;
+    case 7: return k_agg_lean<2, 1, 1, 1>;
+    default: return nullptr;
+  }
+}
+}  // namespace pac

@@ -13,9 +13,14 @@ name, extra = sys.argv[1], sys.argv[2:]
 out_dir = os.path.join(ROOT, "build", "variants", name)
 os.makedirs(out_dir, exist_ok=True)
 srcs = sorted(glob.glob(os.path.join(ROOT, "paper_2603_15023_b200", "csrc", "*.cu")))
+# ONLY=pattern: recompile only the matching sources, link the rest from the default build
+only = os.environ.get("ONLY")
+default_objs = os.path.join(ROOT, "build", "libpac")
 
 
 def one(src):
+    if only and only not in os.path.basename(src):
+        return os.path.join(default_objs, os.path.basename(src) + ".o")
     obj = os.path.join(out_dir, os.path.basename(src) + ".o")
     cmd = [B.NVCC] + B.ARCH + B.NVFLAGS + extra + ["-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]
     r = subprocess.run(cmd, capture_output=True, text=True)
