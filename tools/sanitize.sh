@@ -16,4 +16,7 @@ for tool in memcheck racecheck; do
   PAC_WS=1 timeout 900 $CS --tool $tool --error-exitcode 9 --print-limit 20 python tools/prof_agg.py --config C5 --rows 40000 --iters 1 \
     > $out/sanitize_${tool}_C5_ws.txt 2>&1
   echo "$tool C5 (PAC_WS=1) rc=$?" | tee -a $out/sanitize_summary.txt
+  PAC_PART=1 timeout 900 $CS --tool $tool --error-exitcode 9 --print-limit 20 python tools/prof_agg.py --config C3 --rows 40000 --iters 1 \
+    > $out/sanitize_${tool}_C3_part.txt 2>&1
+  echo "$tool C3 (PAC_PART=1) rc=$?" | tee -a $out/sanitize_summary.txt
 done
