@@ -920,7 +920,7 @@ __global__ void k_gather(AggPlan p, const int* Gdev, const int* perm, pac_table 
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   for (int rank = blockIdx.x * wpb + (threadIdx.x >> 5); rank < G; rank += gridDim.x * wpb) {
-    const int prov = perm[rank];
+    const int prov = perm ? perm[rank] : rank;  // NULL: the provisional slots are canonical (sort-first path)
     const size_t pb = (size_t)prov * kM, ob = (size_t)rank * kM;
     uint64_t K = 0;
     if (p.has_count) {
@@ -1404,6 +1404,18 @@ int part_rows(const void* const* src, const int* eb, int ncol, int hash0, uint64
 constexpr int kPartUnitRows = 32768;    // rows per unit (a multiple of the tile rows)
 constexpr int64_t kPartMinRows = 1 << 20;
 
+// Sort-first (sortagg.cu): rows radix-sorted by packed key, then one streaming 64-world fold
+size_t srt_ws_bytes(int64_t n_rows, int nv, int sms);
+int srt_run(const AggPlan& p, const int64_t* d_pu_key, const uint64_t* d_mask, const pac_key_col* keys, int n_keys,
+            int width, int64_t n_rows, int sms, char* ws, cudaStream_t st);
+constexpr int64_t kSrtMinGroups = 4096;  // below: the tile kernels (CTA-local slots catch most rows)
+static bool srt_applicable(const AccSet& A, int n_keys, int width, int64_t G_cap, int64_t n_rows) {
+  if (getenv("PAC_NO_SORT") || getenv("PAC_PART") || !A.has_count || A.has_min || A.has_max || n_keys < 1 || width > 4 || n_rows < 1 ||
+      n_rows >= ((int64_t)1 << 31))
+    return false;
+  return G_cap >= kSrtMinGroups || (getenv("PAC_SORT") && G_cap > 128);
+}
+
 // Partition-first (opt-in, PAC_PART=1: measured slower than the deferred tier on C3)
 // applies to large inputs whose table has many more groups than the TMEM CTA table holds
 // (G_cap >= 4 Lcap); P = 2^pbits partitions of <= Lcap / 2 groups by capacity.
@@ -1464,6 +1476,8 @@ extern "C" int pac_agg_workspace_size_rows(const pac_agg_spec* aggs, int n_aggs,
   *bytes = spill_layout(A, G_cap, base, std::min<int64_t>(spill_rows_needed(n_rows), INT32_MAX - 1)).bytes + 4 * 256;
   int pbits = 0;
   if (want_partition(G_cap, n_rows, L, &pbits)) *bytes = std::max(*bytes, base + part_ws_for(A, n_rows, pbits, sms));
+  // sort-first (key width unknown here: sized for keys of <= 4 bytes, which are the ones it takes)
+  if (srt_applicable(A, 1, 4, G_cap, n_rows)) *bytes = std::max(*bytes, base + srt_ws_bytes(n_rows, A.ni + A.nf, sms));
   return PAC_OK;
 }
 
@@ -1570,6 +1584,7 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
 
   if (int rc2 = plan_reset(A, W, ws, n_aggs, st)) return rc2;
   cudaError_t e = cudaSuccess;
+  bool sorted = false;  // sort-first path: provisional slots already in canonical order
   if (n_rows > 0) {
     if (!A.has_count) {
       MMLayout L = mm_layout(G_cap, smem_max);
@@ -1630,6 +1645,14 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
       char kname[64];
       e = launch_lean(p, n_keys, width, sms, st, kname, (int)sizeof(kname));  // opens the profile region
       profile_end(st);
+    } else if (srt_applicable(A, n_keys, width, G_cap, n_rows) &&
+               ws_bytes >= W.bytes + srt_ws_bytes(n_rows, A.ni + A.nf, sms)) {
+      // high cardinality: rows radix-sorted by key, then a streaming fold (sortagg.cu)
+      profile_begin(st, "k_srt_{hist,scan,scatter} x passes + k_srt_{heads,hscan,bzero,agg}");
+      const int src = srt_run(p, d_pu_key, d_mask, keys, n_keys, width, n_rows, sms, ws + W.bytes, st);
+      profile_end(st);
+      if (src != PAC_OK) return src;
+      sorted = true;
     } else {
       SmemLayout L{};
       if (!choose_layout(A, G_cap, smem_max, width, &L)) return PAC_E_INVAL;
@@ -1747,7 +1770,9 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
   }
   k_finish_count<<<1, 1, 0, st>>>(p, n_keys, out->d_num_groups, out->d_status, Gdev);
   note_launch();
-  if (G_cap <= kSmallSort) {
+  if (sorted) {
+    perm = nullptr;  // identity
+  } else if (G_cap <= kSmallSort) {
     k_sort_small<<<1, 1024, 0, st>>>(p.prov_key, Gdev, perm);
     note_launch();
   } else {
