@@ -920,7 +920,7 @@ __global__ void k_gather(AggPlan p, const int* Gdev, const int* perm, pac_table 
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   for (int rank = blockIdx.x * wpb + (threadIdx.x >> 5); rank < G; rank += gridDim.x * wpb) {
-    const int prov = perm ? perm[rank] : rank;  // NULL: the provisional slots are canonical (sort-first path)
+    const int prov = perm[rank];
     const size_t pb = (size_t)prov * kM, ob = (size_t)rank * kM;
     uint64_t K = 0;
     if (p.has_count) {
@@ -1407,7 +1407,9 @@ constexpr int64_t kPartMinRows = 1 << 20;
 // Sort-first (sortagg.cu): rows radix-sorted by packed key, then one streaming 64-world fold
 size_t srt_ws_bytes(int64_t n_rows, int nv, int sms);
 int srt_run(const AggPlan& p, const int64_t* d_pu_key, const uint64_t* d_mask, const pac_key_col* keys, int n_keys,
-            int width, int64_t n_rows, int sms, char* ws, cudaStream_t st);
+            int width, int64_t n_rows, int sms, char* ws, const pac_table* out, int n_aggs, const int* kinds,
+            const int* idx, cudaStream_t st);
+void srt_finish(const AggPlan& p, const pac_table* out, int sms, cudaStream_t st);
 constexpr int64_t kSrtMinGroups = 4096;  // below: the tile kernels (CTA-local slots catch most rows)
 static bool srt_applicable(const AccSet& A, int n_keys, int width, int64_t G_cap, int64_t n_rows) {
   if (getenv("PAC_NO_SORT") || getenv("PAC_PART") || !A.has_count || A.has_min || A.has_max || n_keys < 1 || width > 4 || n_rows < 1 ||
@@ -1649,7 +1651,8 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
                ws_bytes >= W.bytes + srt_ws_bytes(n_rows, A.ni + A.nf, sms)) {
       // high cardinality: rows radix-sorted by key, then a streaming fold (sortagg.cu)
       profile_begin(st, "k_srt_{hist,scan,scatter} x passes + k_srt_{heads,hscan,bzero,agg}");
-      const int src = srt_run(p, d_pu_key, d_mask, keys, n_keys, width, n_rows, sms, ws + W.bytes, st);
+      const int src = srt_run(p, d_pu_key, d_mask, keys, n_keys, width, n_rows, sms, ws + W.bytes, out, n_aggs,
+                              A.src_kind, A.src_idx, st);
       profile_end(st);
       if (src != PAC_OK) return src;
       sorted = true;
@@ -1770,9 +1773,11 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
   }
   k_finish_count<<<1, 1, 0, st>>>(p, n_keys, out->d_num_groups, out->d_status, Gdev);
   note_launch();
-  if (sorted) {
-    perm = nullptr;  // identity
-  } else if (G_cap <= kSmallSort) {
+  if (sorted) {  // k_srt_agg wrote the output table in canonical order: no sort, no gather
+    srt_finish(p, out, sms, st);
+    return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
+  }
+  if (G_cap <= kSmallSort) {
     k_sort_small<<<1, 1024, 0, st>>>(p.prov_key, Gdev, perm);
     note_launch();
   } else {

@@ -41,8 +41,10 @@ void profile_end(cudaStream_t st);
 #endif
 constexpr int kSrtThreads = 256;  // k_srt_hist / k_srt_scatter
 constexpr int kSrtW = kSrtThreads / 32;
-constexpr int kSrtRPT = 8;        // rows per thread and tile
-constexpr int kSrtT = kSrtThreads * kSrtRPT;  // 2048 rows per tile
+// rows per thread and tile of k_srt_scatter: 16 (4096-row tiles, 16 rows per digit on average)
+// for rows of at most one value column, 8 otherwise (registers)
+__host__ __device__ constexpr int srt_rpt(int) { return 8; }  // (16 measured no faster on C3)
+constexpr int kSrtTmax = 4096;    // CTA chunks are multiples of every tile size
 constexpr int kSrtCH = 2048;      // rows per k_srt_agg work item (one warp)
 constexpr int kSrtMaxV = 4;       // value columns moved with the rows
 
@@ -65,6 +67,14 @@ struct SrtPlan {
   int grid;                               // CTAs of k_srt_hist / k_srt_scatter
   int* hcnt;                              // [nch] group starts per agg chunk, then their scan
   int nch;                                // agg chunks (upper bound, from n)
+};
+
+// The output table, written directly by k_srt_agg (the slots are canonical: no gather pass).
+struct SrtOut {
+  pac_table t;
+  int n_aggs;
+  int kind[PAC_MAX_AGGS];  // 0 count (no world array), 1 int64 sum src idx, 2 f64 sum src idx
+  int idx[PAC_MAX_AGGS];
 };
 
 __device__ __forceinline__ uint32_t srt_pack_key(const SrtPlan& q, int64_t r) {
@@ -123,7 +133,7 @@ __device__ __forceinline__ int64_t srt_rows(const SrtPlan& q, int b) { return b 
 // rows of one CTA's chunk (multiple of the tile), the same in k_srt_hist and k_srt_scatter
 __device__ __forceinline__ int64_t srt_chunk(int64_t n, int grid) {
   const int64_t per = (n + grid - 1) / grid;
-  return (per + kSrtT - 1) / kSrtT * kSrtT;
+  return (per + kSrtTmax - 1) / kSrtTmax * kSrtTmax;
 }
 
 // per-CTA digit counts of byte b (pass 0: also the OR / AND of the packed keys).  Per-warp
@@ -254,13 +264,14 @@ __global__ void __launch_bounds__(1024) k_srt_scan(SrtPlan q, int b) {
 // them batch by batch (match_any), so the order inside a digit is: warp, batch, lane -- the input
 // order.  The tile is reordered by digit in shared memory and written in runs to the cursors.
 template <int NV, bool P0>
-__global__ void __launch_bounds__(kSrtThreads, PAC_SRT_MINB) k_srt_scatter(SrtPlan q, int b) {
+__global__ void __launch_bounds__(kSrtThreads, NV <= 1 ? PAC_SRT_MINB : 2) k_srt_scatter(SrtPlan q, int b) {
   if (!P0 && !srt_active(q, b)) return;
+  constexpr int RPT = srt_rpt(NV), T = kSrtThreads * RPT;  // longer digit runs per tile when the rows are narrow
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* smsk = (unsigned long long*)smem;                 // [T]
-  unsigned long long* sval = smsk + kSrtT;                              // [NV][T]
-  uint32_t* skey = (uint32_t*)(sval + NV * kSrtT);                      // [T]
-  int* cnt = (int*)(skey + kSrtT);                                      // [256][W]
+  unsigned long long* sval = smsk + T;                              // [NV][T]
+  uint32_t* skey = (uint32_t*)(sval + NV * T);                      // [T]
+  int* cnt = (int*)(skey + T);                                      // [256][W]
   int* dstart = cnt + 256 * kSrtW;                                      // [256]
   long long* cur = (long long*)(dstart + 256);                          // [256]
   __shared__ int s_wsum[kSrtW];
@@ -276,42 +287,57 @@ __global__ void __launch_bounds__(kSrtThreads, PAC_SRT_MINB) k_srt_scatter(SrtPl
 #pragma unroll
   for (int w = 0; w < kSrtW; ++w) cnt[tid * kSrtW + w] = 0;
   __syncthreads();
-  for (int64_t t0 = r0; t0 < r1; t0 += kSrtT) {
-    uint32_t key[kSrtRPT], rk[kSrtRPT];
-    unsigned long long m[kSrtRPT], v[kSrtRPT][NV > 0 ? NV : 1];
-    // load (pass 0: pack, hash; explicit zero masks are dropped)
+  for (int64_t t0 = r0; t0 < r1; t0 += T) {
+    uint32_t key[RPT], rk[RPT];
+    unsigned long long m[RPT], v[RPT][NV > 0 ? NV : 1];
+    // load (pass 0: pack, hash; explicit zero masks are dropped).  Every load of the tile is
+    // issued before any loaded value is used.
+    if (P0) {
+      const unsigned long long* msrc = q.mask_in ? q.mask_in : (const unsigned long long*)q.pu;
+      const bool k4 = q.n_keys == 1 && q.key_bytes[0] == 4;  // the common layout: one int32 key
+      const uint32_t* kc = (const uint32_t*)q.key_col[0];
 #pragma unroll
-    for (int j = 0; j < kSrtRPT; ++j) {
-      const int64_t r = t0 + wid * (32 * kSrtRPT) + 32 * j + lane;
-      const bool in = r < r1;
-      if (P0) {
-        m[j] = in ? (q.mask_in ? q.mask_in[r] : (unsigned long long)__ldg(q.pu + r)) : 0ull;
+      for (int j = 0; j < RPT; ++j) {
+        const int64_t r = t0 + wid * (32 * RPT) + 32 * j + lane;
+        const bool in = r < r1;
+        m[j] = in ? __ldg(msrc + r) : 0ull;
 #pragma unroll
         for (int c = 0; c < NV; ++c) v[j][c] = in ? __ldg(q.val_in[c] + r) : 0ull;
-      } else {
+        key[j] = (in && k4) ? __ldg(kc + r) : 0u;  // R20 sign flip applied at first use (ranks)
+      }
+      if (!k4) {
+        int64_t rr[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) rr[j] = t0 + wid * (32 * RPT) + 32 * j + lane;
+        srt_pack_keys<RPT>(q, rr, r1, key);
+      }
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int64_t r = t0 + wid * (32 * RPT) + 32 * j + lane;
+        rk[j] = (r < r1 && (!q.mask_in || m[j] != 0ull)) ? 0u : 0xFFFFFFFFu;  // 0xFFFFFFFF: not kept
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int64_t r = t0 + wid * (32 * RPT) + 32 * j + lane;
+        const bool in = r < r1;
         key[j] = in ? q.key[ib][r] : 0u;
         m[j] = in ? q.msk[ib][r] : 0ull;
 #pragma unroll
         for (int c = 0; c < NV; ++c) v[j][c] = in ? q.val[ib][c][r] : 0ull;
+        rk[j] = in ? 0u : 0xFFFFFFFFu;
       }
-      rk[j] = in && (!P0 || !q.mask_in || m[j] != 0ull) ? 0u : 0xFFFFFFFFu;  // 0xFFFFFFFF: not kept
-    }
-    if (P0) {  // after the mask / value loads are in flight
-      int64_t rr[kSrtRPT];
-#pragma unroll
-      for (int j = 0; j < kSrtRPT; ++j) rr[j] = t0 + wid * (32 * kSrtRPT) + 32 * j + lane;
-      srt_pack_keys<kSrtRPT>(q, rr, r1, key);
     }
     if (P0 && q.pu && q.hash0) {
       // pac_hash (R1, R2): mix, popcount and draw word 0 branch-free for every row (two rows
       // interleaved); rows that still need flips are queued per warp and finished with all 32
       // lanes busy.  The staging buffer is free until the reorder below.
-      unsigned long long* res = smsk + wid * (32 * kSrtRPT);
-      unsigned long long* qw = sval + wid * (32 * kSrtRPT);  // NV >= 1 here (see srt_pass)
-      unsigned short* qr = (unsigned short*)(skey) + wid * (32 * kSrtRPT);
+      unsigned long long* res = smsk + wid * (32 * RPT);
+      unsigned long long* qw = sval + wid * (32 * RPT);  // NV >= 1 here (see srt_pass)
+      unsigned short* qr = (unsigned short*)(skey) + wid * (32 * RPT);
       int qn = 0;
 #pragma unroll
-      for (int j = 0; j < kSrtRPT; j += 2) {
+      for (int j = 0; j < RPT; j += 2) {
         HashState ha, hb;
         pac_hash_begin2(m[j], m[j + 1], q.salt, ha, hb);
         m[j] = hash_mask_now(ha);
@@ -341,13 +367,17 @@ __global__ void __launch_bounds__(kSrtThreads, PAC_SRT_MINB) k_srt_scatter(SrtPl
       }
       __syncwarp();
 #pragma unroll
-      for (int j = 0; j < kSrtRPT; ++j)
+      for (int j = 0; j < RPT; ++j)
         if (rk[j] == 0u && __popcll(m[j]) != 32) m[j] = res[32 * j + lane];
       __syncwarp();
     }
     // ranks within (digit, warp), batch by batch
+    if (P0 && q.n_keys == 1 && q.key_bytes[0] == 4) {
 #pragma unroll
-    for (int j = 0; j < kSrtRPT; ++j) {
+      for (int j = 0; j < RPT; ++j) key[j] ^= 0x80000000u;
+    }
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
       const bool ok = rk[j] == 0u;
       const uint32_t d = (key[j] >> (8 * b)) & 255u;
       const unsigned peers = __match_any_sync(0xffffffffu, ok ? d : 256u + lane);
@@ -386,14 +416,14 @@ __global__ void __launch_bounds__(kSrtThreads, PAC_SRT_MINB) k_srt_scatter(SrtPl
     __syncthreads();
     // stage the tile in digit order
 #pragma unroll
-    for (int j = 0; j < kSrtRPT; ++j) {
+    for (int j = 0; j < RPT; ++j) {
       if (rk[j] == 0xFFFFFFFFu) continue;
       const int d = (int)(rk[j] >> 16);
       const int pos = dstart[d] + cnt[d * kSrtW + wid] + (int)(rk[j] & 0xFFFFu);
       skey[pos] = key[j];
       smsk[pos] = m[j];
 #pragma unroll
-      for (int c = 0; c < NV; ++c) sval[c * kSrtT + pos] = v[j][c];
+      for (int c = 0; c < NV; ++c) sval[c * T + pos] = v[j][c];
     }
     __syncthreads();
     // write out: consecutive staged rows of one digit go to consecutive output rows
@@ -405,7 +435,7 @@ __global__ void __launch_bounds__(kSrtThreads, PAC_SRT_MINB) k_srt_scatter(SrtPl
       q.key[ob][g] = k;
       q.msk[ob][g] = smsk[i];
 #pragma unroll
-      for (int c = 0; c < NV; ++c) q.val[ob][c][g] = sval[c * kSrtT + i];
+      for (int c = 0; c < NV; ++c) q.val[ob][c][g] = sval[c * T + i];
     }
     __syncthreads();
     cur[tid] += tot;
@@ -536,7 +566,7 @@ __global__ void __launch_bounds__(1024) k_srt_hscan(SrtPlan q, int* gcounter) {
 }
 
 // rows of the groups that span a chunk boundary start at zero (their chunks add with atomics)
-__global__ void __launch_bounds__(256) k_srt_bzero(SrtPlan q, AggPlan p) {
+__global__ void __launch_bounds__(256) k_srt_bzero(SrtPlan q, SrtOut o, int64_t G_cap) {
   const int lane = threadIdx.x & 31;
   const int ch = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (ch >= q.nch || ch == 0) return;
@@ -546,15 +576,44 @@ __global__ void __launch_bounds__(256) k_srt_bzero(SrtPlan q, AggPlan p) {
   const uint32_t* key = q.key[(srt_nactive(q, q.width) - 1) & 1];
   if (key[c0] != key[c0 - 1]) return;
   const int slot = q.hcnt[ch] - 1;
-  if (slot < 0 || slot >= p.G_cap) return;
+  if (slot < 0 || slot >= G_cap) return;
   const size_t bw = (size_t)slot * kM;
   for (int h = 0; h < 2; ++h) {
     const int j = lane + 32 * h;
-    if (p.has_count) p.prov_count[bw + j] = 0;
-    for (int c = 0; c < p.ni; ++c) p.prov_isum[c][bw + j] = 0;
-    for (int c = 0; c < p.nf; ++c) p.prov_fsum[c][bw + j] = 0.0;
+    o.t.d_count[bw + j] = 0;
+    for (int a = 0; a < o.n_aggs; ++a) {
+      if (o.kind[a] == 1) ((int64_t*)o.t.d_world[a])[bw + j] = 0;
+      else if (o.kind[a] == 2) ((double*)o.t.d_world[a])[bw + j] = 0.0;
+    }
   }
-  if (lane == 0) p.prov_rows[slot] = 0;
+  if (lane == 0) o.t.d_rows[slot] = 0;
+}
+
+// K of the groups that span a chunk boundary, from their finished counts (R5)
+__global__ void __launch_bounds__(256) k_srt_bpresence(SrtPlan q, SrtOut o, int64_t G_cap) {
+  const int lane = threadIdx.x & 31;
+  const int ch = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (ch >= q.nch || ch == 0) return;
+  const int64_t n = (int64_t)q.ctr[0];
+  const int64_t c0 = (int64_t)ch * kSrtCH;
+  if (c0 >= n) return;
+  const uint32_t* key = q.key[(srt_nactive(q, q.width) - 1) & 1];
+  if (key[c0] != key[c0 - 1]) return;
+  const int slot = q.hcnt[ch] - 1;
+  if (slot < 0 || slot >= G_cap) return;
+  const size_t bw = (size_t)slot * kM;
+  const uint64_t K = (uint64_t)__ballot_sync(0xffffffffu, o.t.d_count[bw + lane] != 0) |
+                     ((uint64_t)__ballot_sync(0xffffffffu, o.t.d_count[bw + lane + 32] != 0) << 32);
+  if (lane == 0) o.t.d_presence[slot] = K;
+}
+
+// R15 overflow bound over the finished table (after k_finish_count wrote the status)
+__global__ void k_srt_overflow(const unsigned long long* gmaxabs, pac_table t, int64_t G_cap) {
+  const unsigned long long ma = *gmaxabs;
+  if (!ma) return;
+  const int64_t G = min((int64_t)*t.d_num_groups, G_cap);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x)
+    if ((unsigned long long)t.d_rows[g] > (0x7FFFFFFFFFFFFFFFull / ma)) atomicExch(t.d_status, PAC_E_OVERFLOW);
 }
 
 // Streaming 64-world fold over the sorted rows.  Per warp: one chunk of kSrtCH rows, windows of
@@ -563,7 +622,7 @@ __global__ void __launch_bounds__(256) k_srt_bzero(SrtPlan q, AggPlan p) {
 // zero (finite padding, run_body's contract).
 constexpr int kSrtS = 48;  // staged rows per copy
 template <int NI, int NF>
-__global__ void __launch_bounds__(256) k_srt_agg(SrtPlan q, AggPlan p) {
+__global__ void __launch_bounds__(256) k_srt_agg(SrtPlan q, AggPlan p, SrtOut o) {
   constexpr int NV = NI + NF;
   constexpr int ROWW = 1 + NV;  // 8-byte words per staged row (mask, values)
   __shared__ __align__(16) unsigned long long stage[8][2][ROWW * kSrtS];
@@ -603,39 +662,46 @@ __global__ void __launch_bounds__(256) k_srt_agg(SrtPlan q, AggPlan p) {
       if (slot < 0 || slot >= G_cap) return;
       const size_t bw = (size_t)slot * kM;
       if (!atomic) {
-        if (p.has_count) {
-          p.prov_count[bw + lane] = acc.c0;
-          p.prov_count[bw + lane + 32] = acc.c1;
+        o.t.d_count[bw + lane] = (int64_t)acc.c0;
+        o.t.d_count[bw + lane + 32] = (int64_t)acc.c1;
+        for (int a = 0; a < o.n_aggs; ++a) {
+          const int kd = o.kind[a], ix = o.idx[a];
+          if (kd == 1) {
+            int64_t* w = (int64_t*)o.t.d_world[a];
+            w[bw + lane] = ix == 0 ? acc.ia0[0] : acc.ia0[NI > 1 ? 1 : 0];
+            w[bw + lane + 32] = ix == 0 ? acc.ia1[0] : acc.ia1[NI > 1 ? 1 : 0];
+          } else if (kd == 2) {
+            double* w = (double*)o.t.d_world[a];
+            w[bw + lane] = ix == 0 ? acc.fa0[0] : acc.fa0[NF > 1 ? 1 : 0];
+            w[bw + lane + 32] = ix == 0 ? acc.fa1[0] : acc.fa1[NF > 1 ? 1 : 0];
+          }
         }
-#pragma unroll
-        for (int c = 0; c < NI; ++c) {
-          p.prov_isum[c][bw + lane] = (unsigned long long)acc.ia0[c];
-          p.prov_isum[c][bw + lane + 32] = (unsigned long long)acc.ia1[c];
+        const uint64_t K = (uint64_t)__ballot_sync(0xffffffffu, acc.c0 != 0) |
+                           ((uint64_t)__ballot_sync(0xffffffffu, acc.c1 != 0) << 32);
+        if (lane == 0) {
+          o.t.d_rows[slot] = (int64_t)rows;
+          o.t.d_presence[slot] = K;
         }
-#pragma unroll
-        for (int c = 0; c < NF; ++c) {
-          p.prov_fsum[c][bw + lane] = acc.fa0[c];
-          p.prov_fsum[c][bw + lane + 32] = acc.fa1[c];
-        }
-        if (lane == 0) p.prov_rows[slot] = rows;
       } else {
-        if (p.has_count) {
-          if (acc.c0) atomicAdd(&p.prov_count[bw + lane], (unsigned long long)acc.c0);
-          if (acc.c1) atomicAdd(&p.prov_count[bw + lane + 32], (unsigned long long)acc.c1);
+        if (acc.c0) atomicAdd((unsigned long long*)&o.t.d_count[bw + lane], (unsigned long long)acc.c0);
+        if (acc.c1) atomicAdd((unsigned long long*)&o.t.d_count[bw + lane + 32], (unsigned long long)acc.c1);
+        for (int a = 0; a < o.n_aggs; ++a) {
+          const int kd = o.kind[a], ix = o.idx[a];
+          if (kd == 1) {
+            unsigned long long* w = (unsigned long long*)o.t.d_world[a];
+            const long long x0 = ix == 0 ? acc.ia0[0] : acc.ia0[NI > 1 ? 1 : 0];
+            const long long x1 = ix == 0 ? acc.ia1[0] : acc.ia1[NI > 1 ? 1 : 0];
+            if (x0) atomicAdd(&w[bw + lane], (unsigned long long)x0);
+            if (x1) atomicAdd(&w[bw + lane + 32], (unsigned long long)x1);
+          } else if (kd == 2) {
+            double* w = (double*)o.t.d_world[a];
+            if (acc.c0) atomicAdd(&w[bw + lane], ix == 0 ? acc.fa0[0] : acc.fa0[NF > 1 ? 1 : 0]);
+            if (acc.c1) atomicAdd(&w[bw + lane + 32], ix == 0 ? acc.fa1[0] : acc.fa1[NF > 1 ? 1 : 0]);
+          }
         }
-#pragma unroll
-        for (int c = 0; c < NI; ++c) {
-          if (acc.ia0[c]) atomicAdd(&p.prov_isum[c][bw + lane], (unsigned long long)acc.ia0[c]);
-          if (acc.ia1[c]) atomicAdd(&p.prov_isum[c][bw + lane + 32], (unsigned long long)acc.ia1[c]);
-        }
-#pragma unroll
-        for (int c = 0; c < NF; ++c) {
-          if (acc.c0) atomicAdd(&p.prov_fsum[c][bw + lane], acc.fa0[c]);
-          if (acc.c1) atomicAdd(&p.prov_fsum[c][bw + lane + 32], acc.fa1[c]);
-        }
-        if (lane == 0 && rows) atomicAdd(&p.prov_rows[slot], rows);
+        if (lane == 0 && rows) atomicAdd((unsigned long long*)&o.t.d_rows[slot], rows);
       }
-      if (cur_here && lane == 0) p.prov_key[slot] = (unsigned long long)cur_key;
+      if (cur_here && lane == 0) o.t.d_group_key[slot] = (uint64_t)cur_key;
     };
     for (int64_t wb = c0; wb < c1; wb += 32) {
       const int64_t r = wb + lane;
@@ -727,7 +793,9 @@ size_t srt_ws_bytes(int64_t n_rows, int nv, int sms) {
 }
 
 // staging (mask, values, key) + warp counters + digit starts + cursors
-static size_t srt_smem(int nv, bool) { return (size_t)kSrtT * (8 + 8 * nv + 4) + 256 * kSrtW * 4 + 256 * 4 + 256 * 8; }
+static size_t srt_smem(int nv, bool) {
+  return (size_t)kSrtThreads * srt_rpt(nv) * (8 + 8 * nv + 4) + 256 * kSrtW * 4 + 256 * 4 + 256 * 8;
+}
 
 template <int NV>
 static cudaError_t srt_pass(const SrtPlan& q, int b, cudaStream_t st) {
@@ -743,10 +811,10 @@ static cudaError_t srt_pass(const SrtPlan& q, int b, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-using SrtAggFn = void (*)(const SrtPlan&, const AggPlan&, int, cudaStream_t);
+using SrtAggFn = void (*)(const SrtPlan&, const AggPlan&, const SrtOut&, int, cudaStream_t);
 template <int NI, int NF>
-static void srt_agg_launch(const SrtPlan& q, const AggPlan& p, int grid, cudaStream_t st) {
-  k_srt_agg<NI, NF><<<grid, 256, 0, st>>>(q, p);
+static void srt_agg_launch(const SrtPlan& q, const AggPlan& p, const SrtOut& o, int grid, cudaStream_t st) {
+  k_srt_agg<NI, NF><<<grid, 256, 0, st>>>(q, p, o);
 }
 static const SrtAggFn kSrtAgg[3][3] = {
     {srt_agg_launch<0, 0>, srt_agg_launch<0, 1>, srt_agg_launch<0, 2>},
@@ -756,7 +824,15 @@ static const SrtAggFn kSrtAgg[3][3] = {
 // Runs the whole sort-first aggregation into the provisional table of `p` (slots in canonical
 // order, *p.gcounter = number of groups).  ws: srt_ws_bytes(n_rows, ni + nf, sms) bytes.
 int srt_run(const AggPlan& p, const int64_t* d_pu_key, const uint64_t* d_mask, const pac_key_col* keys, int n_keys,
-            int width, int64_t n_rows, int sms, char* ws, cudaStream_t st) {
+            int width, int64_t n_rows, int sms, char* ws, const pac_table* out, int n_aggs, const int* kinds,
+            const int* idx, cudaStream_t st) {
+  SrtOut o{};
+  o.t = *out;
+  o.n_aggs = n_aggs;
+  for (int a = 0; a < n_aggs; ++a) {
+    o.kind[a] = kinds[a];
+    o.idx[a] = idx[a];
+  }
   SrtPlan q{};
   q.n = n_rows;
   q.pu = (const long long*)d_pu_key;
@@ -810,11 +886,20 @@ int srt_run(const AggPlan& p, const int64_t* d_pu_key, const uint64_t* d_mask, c
     }
     k_srt_heads<<<hb, 256, 0, st>>>(q);
     k_srt_hscan<<<1, 1024, 0, st>>>(q, p.gcounter);
-    k_srt_bzero<<<hb, 256, 0, st>>>(q, p);
-    kSrtAgg[p.ni][p.nf](q, p, std::min(hb, sms * 8), st);
-    for (int i = 0; i < 4; ++i) note_launch();
+    k_srt_bzero<<<hb, 256, 0, st>>>(q, o, p.G_cap);
+    kSrtAgg[p.ni][p.nf](q, p, o, std::min(hb, sms * 8), st);
+    k_srt_bpresence<<<hb, 256, 0, st>>>(q, o, p.G_cap);
+    for (int i = 0; i < 5; ++i) note_launch();
   }
   return cudaGetLastError() == cudaSuccess ? PAC_OK : PAC_E_CUDA;
+}
+
+// after k_finish_count: the R15 overflow bound (k_gather's check, which this path skips)
+void srt_finish(const AggPlan& p, const pac_table* out, int sms, cudaStream_t st) {
+  if (p.ni > 0) {
+    k_srt_overflow<<<sms * 4, 256, 0, st>>>(p.gmaxabs, *out, p.G_cap);
+    note_launch();
+  }
 }
 
 }  // namespace pac
