@@ -219,45 +219,76 @@ __global__ void __launch_bounds__(kSrtThreads) k_srt_hist(SrtPlan q, int b) {
   }
 }
 
-// exclusive scan of hist in digit-major order, in place (one CTA; thread t: digit t / 4, a quarter
-// of the CTAs); pass 0 also counts the rows kept
+// exclusive scan of hist in digit-major order, in place (one CTA of 32 warps).  Warp w owns
+// digits 8w .. 8w+7; per digit all of its CTA counts are loaded at once (coalesced, in flight
+// together), scanned with shuffles, then the digit bases come from a scan of the 256 totals.
+constexpr int kScanMaxGrid = 512;
 __global__ void __launch_bounds__(1024) k_srt_scan(SrtPlan q, int b) {
   if (!srt_active(q, b)) return;
-  __shared__ long long ws[32];
+  __shared__ long long tot[256];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int d = tid >> 2, part = tid & 3, G = q.grid;
-  const int c0 = (G * part) / 4, c1 = (G * (part + 1)) / 4;
-  long long* hd = q.hist + (size_t)d * G;
-  long long s = 0;
-#pragma unroll 8
-  for (int c = c0; c < c1; ++c) s += hd[c];
-  // inclusive scan over the 1024 spans in (digit, part) order = digit-major order
-  long long x = s;
+  const int G = q.grid;
+  constexpr int KMAX = kScanMaxGrid / 32;
+  long long dsum[8];
+#pragma unroll 1
+  for (int i = 0; i < 8; ++i) {  // exclusive within the digit, written back; the digit total kept
+    long long* hd = q.hist + (size_t)(8 * wid + i) * G;
+    long long v[KMAX];
 #pragma unroll
-  for (int k = 1; k < 32; k <<= 1) {
-    const long long y = __shfl_up_sync(0xffffffffu, x, k);
-    if (lane >= k) x += y;
-  }
-  if (lane == 31) ws[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    long long v = ws[lane];
+    for (int k = 0; k < KMAX; ++k) v[k] = (32 * k + lane < G) ? hd[32 * k + lane] : 0;
+    long long carry = 0;
 #pragma unroll
-    for (int k = 1; k < 32; k <<= 1) {
-      const long long y = __shfl_up_sync(0xffffffffu, v, k);
-      if (lane >= k) v += y;
+    for (int k = 0; k < KMAX; ++k) {
+      long long x = v[k];
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, x, s);
+        if (lane >= s) x += y;
+      }
+      const long long all = __shfl_sync(0xffffffffu, x, 31);
+      if (32 * k + lane < G) hd[32 * k + lane] = carry + x - v[k];
+      carry += all;
     }
-    ws[lane] = v;
+    dsum[i] = carry;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tot[8 * wid + i] = dsum[i];
   }
   __syncthreads();
-  long long run = (wid > 0 ? ws[wid - 1] : 0) + x - s;
-#pragma unroll 8
-  for (int c = c0; c < c1; ++c) {
-    const long long v = hd[c];
-    hd[c] = run;
-    run += v;
+  if (wid == 0) {  // digit bases: exclusive scan of the 256 totals (8 per lane)
+    long long t[8], s8 = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      t[i] = tot[8 * lane + i];
+      s8 += t[i];
+    }
+    long long x = s8;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x, s);
+      if (lane >= s) x += y;
+    }
+    long long run = x - s8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      tot[8 * lane + i] = run;
+      run += t[i];
+    }
+    if (lane == 31 && b == 0) q.ctr[0] = (unsigned long long)x;
   }
-  if (b == 0 && tid == 1023) q.ctr[0] = (unsigned long long)ws[31];
+  __syncthreads();
+#pragma unroll 1
+  for (int i = 0; i < 8; ++i) {
+    long long* hd = q.hist + (size_t)(8 * wid + i) * G;
+    const long long base = tot[8 * wid + i];
+    long long v[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) v[k] = (32 * k + lane < G) ? hd[32 * k + lane] : 0;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      if (32 * k + lane < G) hd[32 * k + lane] = base + v[k];
+  }
 }
 
 // One stable counting pass on byte b.  Warp w of a tile owns rows [256 w, 256 w + 256) and ranks
@@ -731,11 +762,12 @@ __global__ void __launch_bounds__(256) k_srt_agg(SrtPlan q, AggPlan p, SrtOut o)
       const bool fin = NF == 0 || __all_sync(0xffffffffu, fi);
       // stage: A[l] = row l, B[l + 1] = row l (masks, then the value columns, stride kSrtS)
       A[lane] = mk;
-      B[lane + 1] = mk;
 #pragma unroll
-      for (int c = 0; c < NV; ++c) {
-        A[(1 + c) * kSrtS + lane] = v[c];
-        B[(1 + c) * kSrtS + lane + 1] = v[c];
+      for (int c = 0; c < NV; ++c) A[(1 + c) * kSrtS + lane] = v[c];
+      if (H & ~1u) {  // a segment may start at an odd row: the shifted copy
+        B[lane + 1] = mk;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) B[(1 + c) * kSrtS + lane + 1] = v[c];
       }
       __syncwarp();
       int s = 0;
@@ -778,7 +810,7 @@ __global__ void __launch_bounds__(256) k_srt_agg(SrtPlan q, AggPlan p, SrtOut o)
 
 // ------------------------------------------------------------------ host
 static size_t srt_al(size_t x) { return (x + 255) & ~(size_t)255; }
-static int srt_grid(int sms) { return 2 * sms; }
+static int srt_grid(int sms) { return std::min(2 * sms, kScanMaxGrid); }
 
 size_t srt_ws_bytes(int64_t n_rows, int nv, int sms) {
   const size_t rows = (size_t)std::max<int64_t>(n_rows, 1);
