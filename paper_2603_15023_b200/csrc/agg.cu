@@ -26,11 +26,64 @@
 namespace pac {
 
 // ------------------------------------------------------------------ k_mask
+// pac_hash (R1, R2) row-parallel.  Each warp takes 256 consecutive keys (8 per lane, coalesced):
+// mix, popcount and draw word 0 branch-free for two keys at a time (pac_hash_begin2); the keys that
+// still need flips are queued per warp and finished with all 32 lanes busy, so no lane loops alone
+// through its later draw words while the other 31 wait.
+constexpr int kMaskR = 8;
 __global__ void __launch_bounds__(256) k_mask(const long long* __restrict__ key, int64_t n,
                                               uint64_t salt, unsigned long long* __restrict__ out) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = pac_hash_dev((uint64_t)__ldg(key + i), salt);
+  __shared__ unsigned long long qm[8][32 * kMaskR], qw[8][32 * kMaskR];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t step = (int64_t)gridDim.x * 256 * kMaskR;
+  for (int64_t b0 = (int64_t)blockIdx.x * 256 * kMaskR + wid * 32 * kMaskR; b0 < n; b0 += step) {
+    unsigned long long x[kMaskR];
+#pragma unroll
+    for (int j = 0; j < kMaskR; ++j) {
+      const int64_t r = b0 + 32 * j + lane;
+      x[j] = r < n ? (unsigned long long)__ldg(key + r) : 0ull;
+    }
+    int qn = 0;
+#pragma unroll
+    for (int j = 0; j < kMaskR; j += 2) {
+      HashState ha, hb;
+      pac_hash_begin2(x[j], x[j + 1], salt, ha, hb);
+      x[j] = hash_mask_now(ha);
+      x[j + 1] = hash_mask_now(hb);
+      const unsigned ba = __ballot_sync(0xffffffffu, ha.k > 0);
+      if (ha.k > 0) {
+        const int qi = qn + __popc(ba & lt);
+        qm[wid][qi] = x[j];
+        qw[wid][qi] = ha.w0;
+      }
+      qn += __popc(ba);
+      const unsigned bb = __ballot_sync(0xffffffffu, hb.k > 0);
+      if (hb.k > 0) {
+        const int qi = qn + __popc(bb & lt);
+        qm[wid][qi] = x[j + 1];
+        qw[wid][qi] = hb.w0;
+      }
+      qn += __popc(bb);
+    }
+    __syncwarp();
+    for (int qi = lane; qi < qn; qi += 32) qm[wid][qi] = pac_hash_continue(qm[wid][qi], qw[wid][qi]);
+    __syncwarp();
+    int qp = 0;  // the queue order again: (pair, a before b, lane)
+#pragma unroll
+    for (int j = 0; j < kMaskR; ++j) {
+      const bool st = __popcll(x[j]) != 32;
+      const unsigned bq = __ballot_sync(0xffffffffu, st);
+      if (st) x[j] = qm[wid][qp + __popc(bq & lt)];
+      qp += __popc(bq);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < kMaskR; ++j) {
+      const int64_t r = b0 + 32 * j + lane;
+      if (r < n) out[r] = x[j];
+    }
+  }
 }
 
 // ------------------------------------------------------------------ k_agg_minmax (pruned)
@@ -1443,7 +1496,7 @@ extern "C" int pac_mask(const int64_t* d_pu_key, int64_t n, uint64_t salt, uint6
   if (n == 0) return PAC_OK;
   int sms = 148, smem = 0;
   if (device_info(&sms, &smem) != PAC_OK) return PAC_E_CUDA;
-  int64_t blocks = (n + 255) / 256;
+  int64_t blocks = (n + 256 * kMaskR - 1) / (256 * kMaskR);
   blocks = std::min<int64_t>(blocks, (int64_t)sms * 8);
   k_mask<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>((const long long*)d_pu_key, n, salt,
                                                           (unsigned long long*)d_mask);

@@ -139,14 +139,15 @@ __device__ __forceinline__ int64_t srt_chunk(int64_t n, int grid) {
 // per-CTA digit counts of byte b (pass 0: also the OR / AND of the packed keys).  Per-warp
 // sub-histograms (no match_any), 4 consecutive rows per thread and step (one 16-byte load of the
 // packed keys after pass 0).
+constexpr int kHistThreads = 1024;  // k_srt_hist: 4x the scatter's threads per chunk (occupancy)
 template <bool P0>
-__global__ void __launch_bounds__(kSrtThreads) k_srt_hist(SrtPlan q, int b) {
+__global__ void __launch_bounds__(kHistThreads) k_srt_hist(SrtPlan q, int b) {
   if (!P0 && !srt_active(q, b)) return;
-  __shared__ int h[kSrtW][256];
+  constexpr int HW = kHistThreads / 32;
+  __shared__ int h[HW][256];
   __shared__ unsigned long long s_or, s_and;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-#pragma unroll
-  for (int w = 0; w < kSrtW; ++w) h[w][tid] = 0;
+  for (int i = tid; i < HW * 256; i += kHistThreads) (&h[0][0])[i] = 0;
   if (tid == 0) {
     s_or = 0;
     s_and = ~0ull;
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kSrtThreads) k_srt_hist(SrtPlan q, int b) {
   const int sh = 8 * b;
   int* hw = h[wid];
   uint32_t o = 0, an = ~0u;
-  for (int64_t rb = r0 + 4 * tid; rb < r1; rb += 4 * kSrtThreads) {
+  for (int64_t rb = r0 + 4 * tid; rb < r1; rb += 4 * kHistThreads) {
     uint32_t k4[4];
     bool ok[4];
     if (P0) {
@@ -209,10 +210,12 @@ __global__ void __launch_bounds__(kSrtThreads) k_srt_hist(SrtPlan q, int b) {
     }
   }
   __syncthreads();
-  int c = 0;
-#pragma unroll
-  for (int w = 0; w < kSrtW; ++w) c += h[w][tid];
-  q.hist[(size_t)tid * gridDim.x + blockIdx.x] = c;
+  if (tid < 256) {
+    int c = 0;
+#pragma unroll 8
+    for (int w = 0; w < HW; ++w) c += h[w][tid];
+    q.hist[(size_t)tid * gridDim.x + blockIdx.x] = c;
+  }
   if (P0 && tid == 0) {
     atomicOr(&q.ctr[1], s_or);
     atomicAnd(&q.ctr[2], s_and);
@@ -810,7 +813,9 @@ __global__ void __launch_bounds__(256) k_srt_agg(SrtPlan q, AggPlan p, SrtOut o)
 
 // ------------------------------------------------------------------ host
 static size_t srt_al(size_t x) { return (x + 255) & ~(size_t)255; }
-static int srt_grid(int sms) { return std::min(2 * sms, kScanMaxGrid); }
+// CTAs of the passes: as many as fit resident (k_srt_scatter: 3 per SM for rows of <= 1 value
+// column, 2 above -- registers), one chunk each
+static int srt_grid(int sms, int nv) { return std::min((nv <= 1 ? PAC_SRT_MINB : 2) * sms, kScanMaxGrid); }
 
 size_t srt_ws_bytes(int64_t n_rows, int nv, int sms) {
   const size_t rows = (size_t)std::max<int64_t>(n_rows, 1);
@@ -819,7 +824,7 @@ size_t srt_ws_bytes(int64_t n_rows, int nv, int sms) {
     b += srt_al(rows * 4) + srt_al(rows * 8);
     for (int c = 0; c < nv; ++c) b += srt_al(rows * 8);
   }
-  b += srt_al((size_t)256 * srt_grid(sms) * 8) + srt_al(64);
+  b += srt_al((size_t)256 * kScanMaxGrid * 8) + srt_al(64);
   b += srt_al(4 * (size_t)((n_rows + kSrtCH - 1) / kSrtCH + 1));
   return b;
 }
@@ -835,8 +840,8 @@ static cudaError_t srt_pass(const SrtPlan& q, int b, cudaStream_t st) {
   auto ks = b == 0 ? k_srt_scatter<NV, true> : k_srt_scatter<NV, false>;
   cudaError_t e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  if (b == 0) k_srt_hist<true><<<q.grid, kSrtThreads, 0, st>>>(q, b);
-  else k_srt_hist<false><<<q.grid, kSrtThreads, 0, st>>>(q, b);
+  if (b == 0) k_srt_hist<true><<<q.grid, kHistThreads, 0, st>>>(q, b);
+  else k_srt_hist<false><<<q.grid, kHistThreads, 0, st>>>(q, b);
   k_srt_scan<<<1, 1024, 0, st>>>(q, b);
   ks<<<q.grid, kSrtThreads, sm, st>>>(q, b);
   for (int i = 0; i < 3; ++i) note_launch();
@@ -892,7 +897,7 @@ int srt_run(const AggPlan& p, const int64_t* d_pu_key, const uint64_t* d_mask, c
     q.msk[k] = (unsigned long long*)take(rows * 8);
     for (int c = 0; c < q.nv; ++c) q.val[k][c] = (unsigned long long*)take(rows * 8);
   }
-  q.grid = srt_grid(sms);
+  q.grid = srt_grid(sms, q.nv);
   q.hist = (long long*)take((size_t)256 * q.grid * 8);
   q.ctr = (unsigned long long*)take(64);
   q.nch = (int)((n_rows + kSrtCH - 1) / kSrtCH);
