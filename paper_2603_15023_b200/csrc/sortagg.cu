@@ -39,6 +39,9 @@ void profile_end(cudaStream_t st);
 #ifndef PAC_SRT_MINB
 #define PAC_SRT_MINB 3  // resident k_srt_scatter CTAs per SM the register allocation targets
 #endif
+#ifndef PAC_SRT_AGG_MINB
+#define PAC_SRT_AGG_MINB 4  // resident k_srt_agg CTAs per SM the register allocation targets
+#endif
 constexpr int kSrtThreads = 256;  // k_srt_hist / k_srt_scatter
 constexpr int kSrtW = kSrtThreads / 32;
 // rows per thread and tile of k_srt_scatter: 16 (4096-row tiles, 16 rows per digit on average)
@@ -656,7 +659,7 @@ __global__ void k_srt_overflow(const unsigned long long* gmaxabs, pac_table t, i
 // zero (finite padding, run_body's contract).
 constexpr int kSrtS = 48;  // staged rows per copy
 template <int NI, int NF>
-__global__ void __launch_bounds__(256) k_srt_agg(SrtPlan q, AggPlan p, SrtOut o) {
+__global__ void __launch_bounds__(256, PAC_SRT_AGG_MINB) k_srt_agg(SrtPlan q, AggPlan p, SrtOut o) {
   constexpr int NV = NI + NF;
   constexpr int ROWW = 1 + NV;  // 8-byte words per staged row (mask, values)
   __shared__ __align__(16) unsigned long long stage[8][2][ROWW * kSrtS];
