@@ -66,9 +66,11 @@ struct SrtPlan {
   unsigned long long* msk[2];
   unsigned long long* val[2][kSrtMaxV];
   long long* hist;                        // [256][grid] counts, then offsets (in place)
+  unsigned long long* dtot;               // [4][256] digit totals per pass (zeroed up front)
   unsigned long long* ctr;                // [0] rows kept, [1] OR of keys, [2] AND of keys
   int grid;                               // CTAs of k_srt_hist / k_srt_scatter
-  int* hcnt;                              // [nch] group starts per agg chunk, then their scan
+  int* hcnt;                              // [nch] group starts before the chunk within its block of 8
+  int* hblk;                              // [nch / 8] group starts per block, then their exclusive scan
   int nch;                                // agg chunks (upper bound, from n)
 };
 
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(kHistThreads) k_srt_hist(SrtPlan q, int b) {
 #pragma unroll 8
     for (int w = 0; w < HW; ++w) c += h[w][tid];
     q.hist[(size_t)tid * gridDim.x + blockIdx.x] = c;
+    if (c) atomicAdd(&q.dtot[256 * b + tid], (unsigned long long)c);
   }
   if (P0 && tid == 0) {
     atomicOr(&q.ctr[1], s_or);
@@ -225,75 +228,39 @@ __global__ void __launch_bounds__(kHistThreads) k_srt_hist(SrtPlan q, int b) {
   }
 }
 
-// exclusive scan of hist in digit-major order, in place (one CTA of 32 warps).  Warp w owns
-// digits 8w .. 8w+7; per digit all of its CTA counts are loaded at once (coalesced, in flight
-// together), scanned with shuffles, then the digit bases come from a scan of the 256 totals.
+// exclusive scan of hist in digit-major order, in place: one warp per digit d -- its base is the
+// sum of the digit totals below d (accumulated by k_srt_hist), then the CTA counts of d are scanned
+// (all of them in flight at once).  Pass 0 also records the rows kept.
 constexpr int kScanMaxGrid = 512;
-__global__ void __launch_bounds__(1024) k_srt_scan(SrtPlan q, int b) {
+__global__ void __launch_bounds__(32) k_srt_scan(SrtPlan q, int b) {
   if (!srt_active(q, b)) return;
-  __shared__ long long tot[256];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int G = q.grid;
+  const int lane = threadIdx.x, d = blockIdx.x, G = q.grid;
+  const unsigned long long* tot = q.dtot + 256 * b;
+  long long base = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = 32 * k + lane;
+    base += i < d ? (long long)tot[i] : 0;
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) base += __shfl_xor_sync(0xffffffffu, base, s);
+  if (b == 0 && d == 255 && lane == 0) q.ctr[0] = (unsigned long long)base + tot[255];
   constexpr int KMAX = kScanMaxGrid / 32;
-  long long dsum[8];
-#pragma unroll 1
-  for (int i = 0; i < 8; ++i) {  // exclusive within the digit, written back; the digit total kept
-    long long* hd = q.hist + (size_t)(8 * wid + i) * G;
-    long long v[KMAX];
+  long long* hd = q.hist + (size_t)d * G;
+  long long v[KMAX];
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k) v[k] = (32 * k + lane < G) ? hd[32 * k + lane] : 0;
-    long long carry = 0;
+  for (int k = 0; k < KMAX; ++k) v[k] = (32 * k + lane < G) ? hd[32 * k + lane] : 0;
+  long long carry = base;
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-      long long x = v[k];
-#pragma unroll
-      for (int s = 1; s < 32; s <<= 1) {
-        const long long y = __shfl_up_sync(0xffffffffu, x, s);
-        if (lane >= s) x += y;
-      }
-      const long long all = __shfl_sync(0xffffffffu, x, 31);
-      if (32 * k + lane < G) hd[32 * k + lane] = carry + x - v[k];
-      carry += all;
-    }
-    dsum[i] = carry;
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) tot[8 * wid + i] = dsum[i];
-  }
-  __syncthreads();
-  if (wid == 0) {  // digit bases: exclusive scan of the 256 totals (8 per lane)
-    long long t[8], s8 = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      t[i] = tot[8 * lane + i];
-      s8 += t[i];
-    }
-    long long x = s8;
+  for (int k = 0; k < KMAX; ++k) {
+    long long x = v[k];
 #pragma unroll
     for (int s = 1; s < 32; s <<= 1) {
       const long long y = __shfl_up_sync(0xffffffffu, x, s);
       if (lane >= s) x += y;
     }
-    long long run = x - s8;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      tot[8 * lane + i] = run;
-      run += t[i];
-    }
-    if (lane == 31 && b == 0) q.ctr[0] = (unsigned long long)x;
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (int i = 0; i < 8; ++i) {
-    long long* hd = q.hist + (size_t)(8 * wid + i) * G;
-    const long long base = tot[8 * wid + i];
-    long long v[KMAX];
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) v[k] = (32 * k + lane < G) ? hd[32 * k + lane] : 0;
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k)
-      if (32 * k + lane < G) hd[32 * k + lane] = base + v[k];
+    if (32 * k + lane < G) hd[32 * k + lane] = carry + x - v[k];
+    carry += __shfl_sync(0xffffffffu, x, 31);
   }
 }
 
@@ -547,33 +514,46 @@ __global__ void __launch_bounds__(256) k_srt_hash(SrtPlan q) {
   }
 }
 
-// group starts (row 0, or key != previous key) per agg chunk of the sorted rows
+// group starts (row 0, or key != previous key) per agg chunk of the sorted rows: warp = chunk,
+// CTA = block of 8 chunks; hcnt[ch] = starts in the block's chunks before ch, hblk = block totals
 __global__ void __launch_bounds__(256) k_srt_heads(SrtPlan q) {
-  const int lane = threadIdx.x & 31;
-  const int ch = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (ch >= q.nch) return;
+  __shared__ int wc[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ch = blockIdx.x * 8 + wid;
   const int64_t n = (int64_t)q.ctr[0];
   const uint32_t* key = q.key[(srt_nactive(q, q.width) - 1) & 1];
   const int64_t c0 = (int64_t)ch * kSrtCH, c1 = min(n, c0 + kSrtCH);
   int h = 0;
-  for (int64_t b = c0; b < c1; b += 32) {
-    const int64_t r = b + lane;
-    bool hd = false;
-    if (r < c1) hd = r == 0 || key[r] != key[r - 1];
-    h += __popc(__ballot_sync(0xffffffffu, hd));
+  if (ch < q.nch) {
+    for (int64_t b = c0; b < c1; b += 32) {
+      const int64_t r = b + lane;
+      bool hd = false;
+      if (r < c1) hd = r == 0 || key[r] != key[r - 1];
+      h += __popc(__ballot_sync(0xffffffffu, hd));
+    }
   }
-  if (lane == 0) q.hcnt[ch] = h;
+  if (lane == 0) wc[wid] = h;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int w = 0; w < 8; ++w) {
+      if (blockIdx.x * 8 + w < q.nch) q.hcnt[blockIdx.x * 8 + w] = run;
+      run += wc[w];
+    }
+    q.hblk[blockIdx.x] = run;
+  }
 }
 
-// exclusive scan of the chunk head counts (one CTA); the group count -> the dictionary counter
+// exclusive scan of the block totals (one CTA); the group count -> the dictionary counter
 __global__ void __launch_bounds__(1024) k_srt_hscan(SrtPlan q, int* gcounter) {
   __shared__ int ws[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int per = (q.nch + 1023) / 1024;
-  const int e0 = min(q.nch, tid * per), e1 = min(q.nch, e0 + per);
+  const int nb = (q.nch + 7) / 8;
+  const int per = (nb + 1023) / 1024;
+  const int e0 = min(nb, tid * per), e1 = min(nb, e0 + per);
   int s = 0;
 #pragma unroll 8
-  for (int i = e0; i < e1; ++i) s += q.hcnt[i];
+  for (int i = e0; i < e1; ++i) s += q.hblk[i];
   int x = s;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -595,12 +575,14 @@ __global__ void __launch_bounds__(1024) k_srt_hscan(SrtPlan q, int* gcounter) {
   int run = (wid > 0 ? ws[wid - 1] : 0) + x - s;
 #pragma unroll 8
   for (int i = e0; i < e1; ++i) {
-    const int c = q.hcnt[i];
-    q.hcnt[i] = run;
+    const int c = q.hblk[i];
+    q.hblk[i] = run;
     run += c;
   }
   if (tid == 1023) *gcounter = ws[31];
 }
+// group starts before chunk ch (after k_srt_hscan)
+__device__ __forceinline__ int srt_chunk_base(const SrtPlan& q, int ch) { return q.hblk[ch >> 3] + q.hcnt[ch]; }
 
 // rows of the groups that span a chunk boundary start at zero (their chunks add with atomics)
 __global__ void __launch_bounds__(256) k_srt_bzero(SrtPlan q, SrtOut o, int64_t G_cap) {
@@ -612,7 +594,7 @@ __global__ void __launch_bounds__(256) k_srt_bzero(SrtPlan q, SrtOut o, int64_t 
   if (c0 >= n) return;
   const uint32_t* key = q.key[(srt_nactive(q, q.width) - 1) & 1];
   if (key[c0] != key[c0 - 1]) return;
-  const int slot = q.hcnt[ch] - 1;
+  const int slot = srt_chunk_base(q, ch) - 1;
   if (slot < 0 || slot >= G_cap) return;
   const size_t bw = (size_t)slot * kM;
   for (int h = 0; h < 2; ++h) {
@@ -636,7 +618,7 @@ __global__ void __launch_bounds__(256) k_srt_bpresence(SrtPlan q, SrtOut o, int6
   if (c0 >= n) return;
   const uint32_t* key = q.key[(srt_nactive(q, q.width) - 1) & 1];
   if (key[c0] != key[c0 - 1]) return;
-  const int slot = q.hcnt[ch] - 1;
+  const int slot = srt_chunk_base(q, ch) - 1;
   if (slot < 0 || slot >= G_cap) return;
   const size_t bw = (size_t)slot * kM;
   const uint64_t K = (uint64_t)__ballot_sync(0xffffffffu, o.t.d_count[bw + lane] != 0) |
@@ -689,7 +671,7 @@ __global__ void __launch_bounds__(256, PAC_SRT_AGG_MINB) k_srt_agg(SrtPlan q, Ag
     const int64_t c1 = min(n, c0 + kSrtCH);
     uint32_t prev = c0 > 0 ? key[c0 - 1] : ~key[0];
     const bool end_cont = c1 < n && key[c1] == key[c1 - 1];
-    int slot = q.hcnt[ch] - 1;  // group of the row before the first head of the chunk
+    int slot = srt_chunk_base(q, ch) - 1;  // group of the row before the first head of the chunk
     bool cur_ok = c0 > 0 && key[c0] == prev;  // a group continuing from the previous chunk
     bool cur_here = false;                   // the current group's first row is in this chunk
     uint32_t cur_key = key[c0];
@@ -827,8 +809,9 @@ size_t srt_ws_bytes(int64_t n_rows, int nv, int sms) {
     b += srt_al(rows * 4) + srt_al(rows * 8);
     for (int c = 0; c < nv; ++c) b += srt_al(rows * 8);
   }
-  b += srt_al((size_t)256 * kScanMaxGrid * 8) + srt_al(64);
+  b += srt_al((size_t)256 * kScanMaxGrid * 8) + srt_al(64) + srt_al(4 * 256 * 8);
   b += srt_al(4 * (size_t)((n_rows + kSrtCH - 1) / kSrtCH + 1));
+  b += srt_al(4 * (size_t)((n_rows + kSrtCH - 1) / kSrtCH / 8 + 2));
   return b;
 }
 
@@ -845,7 +828,7 @@ static cudaError_t srt_pass(const SrtPlan& q, int b, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   if (b == 0) k_srt_hist<true><<<q.grid, kHistThreads, 0, st>>>(q, b);
   else k_srt_hist<false><<<q.grid, kHistThreads, 0, st>>>(q, b);
-  k_srt_scan<<<1, 1024, 0, st>>>(q, b);
+  k_srt_scan<<<256, 32, 0, st>>>(q, b);
   ks<<<q.grid, kSrtThreads, sm, st>>>(q, b);
   for (int i = 0; i < 3; ++i) note_launch();
   return cudaGetLastError();
@@ -903,8 +886,11 @@ int srt_run(const AggPlan& p, const int64_t* d_pu_key, const uint64_t* d_mask, c
   q.grid = srt_grid(sms, q.nv);
   q.hist = (long long*)take((size_t)256 * q.grid * 8);
   q.ctr = (unsigned long long*)take(64);
+  q.dtot = (unsigned long long*)take(4 * 256 * 8);
+  if (cudaMemsetAsync(q.dtot, 0, 4 * 256 * 8, st) != cudaSuccess) return PAC_E_CUDA;
   q.nch = (int)((n_rows + kSrtCH - 1) / kSrtCH);
   q.hcnt = (int*)take(4 * (size_t)(q.nch + 1));
+  q.hblk = (int*)take(4 * (size_t)(q.nch / 8 + 2));
   const unsigned long long init[3] = {0ull, 0ull, ~0ull};
   if (cudaMemcpyAsync(q.ctr, init, sizeof(init), cudaMemcpyHostToDevice, st) != cudaSuccess) return PAC_E_CUDA;
   for (int b = 0; b < width; ++b) {
