@@ -154,7 +154,12 @@ int pac_agg_workspace_size(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, 
  * device atomics each.  Equal to pac_agg_workspace_size when no row can miss (G_cap within
  * the local slot capacity, or MIN/MAX-only aggregates).  pac_agg_grouped uses whatever room
  * beyond the minimum ws_bytes offers (capacity ~ (ws_bytes - minimum) / record size rows);
- * rows beyond the capacity fall back to atomics, results identical.  Queries the device. */
+ * rows beyond the capacity fall back to atomics, results identical.  Queries the device.
+ * Sort-first path (high cardinality, DESIGN.md §5 "k_srt_*"): for COUNT / SUM / AVG tables with
+ * G_cap >= 4096 whose packed key is at most 4 bytes, pac_agg_grouped instead radix-sorts the rows
+ * by key when ws_bytes also holds two row buffers, 2 x (4 + 8 + 8 x value columns) bytes per
+ * row; this function returns at least that.  With less workspace the tile kernels + deferred
+ * tier run (identical integers; f64 sums differ only in summation order, R34). */
 int pac_agg_workspace_size_rows(const pac_agg_spec* aggs, int n_aggs, int64_t G_cap, int64_t n_rows,
                                 size_t* bytes);
 
