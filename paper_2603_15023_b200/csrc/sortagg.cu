@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kHistThreads) k_srt_hist(SrtPlan q, int b) {
   const int sh = 8 * b;
   int* hw = h[wid];
   uint32_t o = 0, an = ~0u;
+#pragma unroll 2
   for (int64_t rb = r0 + 4 * tid; rb < r1; rb += 4 * kHistThreads) {
     uint32_t k4[4];
     bool ok[4];
@@ -525,6 +526,7 @@ __global__ void __launch_bounds__(256) k_srt_heads(SrtPlan q) {
   const int64_t c0 = (int64_t)ch * kSrtCH, c1 = min(n, c0 + kSrtCH);
   int h = 0;
   if (ch < q.nch) {
+#pragma unroll 8
     for (int64_t b = c0; b < c1; b += 32) {
       const int64_t r = b + lane;
       bool hd = false;
@@ -641,7 +643,7 @@ __global__ void k_srt_overflow(const unsigned long long* gmaxabs, pac_table t, i
 // zero (finite padding, run_body's contract).
 constexpr int kSrtS = 48;  // staged rows per copy
 template <int NI, int NF>
-__global__ void __launch_bounds__(256, PAC_SRT_AGG_MINB) k_srt_agg(SrtPlan q, AggPlan p, SrtOut o) {
+__global__ void __launch_bounds__(256, NI + NF <= 1 ? PAC_SRT_AGG_MINB : 2) k_srt_agg(SrtPlan q, AggPlan p, SrtOut o) {
   constexpr int NV = NI + NF;
   constexpr int ROWW = 1 + NV;  // 8-byte words per staged row (mask, values)
   __shared__ __align__(16) unsigned long long stage[8][2][ROWW * kSrtS];
