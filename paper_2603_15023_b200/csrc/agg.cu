@@ -94,14 +94,29 @@ constexpr int kMMQueue = 64;  // k_agg_minmax_v: candidate rows queued per warp
 constexpr int kMMHintEvery = PAC_MM_HINT_EVERY;  // tiles between pulls of the per-slot bound hints
 struct MMLayout {
   int Lcap, LH;
-  int o_lkey, o_lstate, o_lprov, o_lrows, o_bmin, o_bmax, o_dirty, o_misc, o_qr, o_qv, o_qp;
+  int o_lkey, o_lstate, o_lprov, o_lrows, o_bmin, o_bmax, o_dirty, o_misc, o_qr, o_qv, o_qp, o_stage;
   int bytes;
 };
+
+// k_agg_minmax_v stages its next tile with cp.async (16-byte LDGSTS per thread: 4 keys + 4 values)
+// while it works on the current one, so the global loads are in flight during the dictionary and
+// bound work instead of stalling it (long_scoreboard); 0 = plain loads at the top of the tile
+#ifndef PAC_MM_STAGE
+#define PAC_MM_STAGE 1
+#endif
+constexpr int kMMStageBytes = 48;  // per thread: int4 keys + 2 x double2 values
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc)
+               : "memory");
+}
 
 #ifndef PAC_MM_LH
 #define PAC_MM_LH 4
 #endif
-__host__ __device__ constexpr MMLayout mm_layout_for(int Lcap) {
+__host__ __device__ constexpr MMLayout mm_layout_for(int Lcap, bool vstage = false) {
+  // vstage (k_agg_minmax_v with PAC_MM_STAGE): no probe-state array (the packed dictionary does
+  // not use it), a per-thread staging area instead -- two CTAs per SM still fit at Lcap = 1024
   MMLayout L{};
   L.Lcap = Lcap;
   L.LH = lay_pow2(PAC_MM_LH * Lcap > 256 ? PAC_MM_LH * Lcap : 256);
@@ -110,13 +125,14 @@ __host__ __device__ constexpr MMLayout mm_layout_for(int Lcap) {
   L.o_lrows = lay_take(off, Lcap * 4);
   L.o_bmin = lay_take(off, Lcap * 8);
   L.o_bmax = lay_take(off, Lcap * 8);
-  L.o_lstate = lay_take(off, L.LH * 4);
+  L.o_lstate = vstage ? 0 : lay_take(off, L.LH * 4);
   L.o_lprov = lay_take(off, Lcap * 4);
   L.o_dirty = lay_take(off, (kThreads / 32) * ((Lcap + 31) / 32) * 4);  // per-warp dirty bitmaps
   L.o_misc = lay_take(off, (int)sizeof(Misc));
   L.o_qr = lay_take(off, (kThreads / 32) * kMMQueue * 8);  // candidate queue: row, value, (prov, slot)
   L.o_qv = lay_take(off, (kThreads / 32) * kMMQueue * 8);
   L.o_qp = lay_take(off, (kThreads / 32) * kMMQueue * 8);
+  L.o_stage = vstage ? lay_take(off, kThreads * kMMStageBytes) : 0;
   L.bytes = off;
   return L;
 }
@@ -417,11 +433,10 @@ __device__ __forceinline__ void mmv_apply(const AggPlan& p, const int64_t* qr, c
 template <int MM, int ROWS, int LC>
 __global__ void __launch_bounds__(kThreads, PAC_MM_MINB) k_agg_minmax_v(AggPlan p, MMLayout Lp) {
   // LC > 0: the layout of LC local slots as a compile-time constant (immediate smem offsets)
-  constexpr MMLayout Lc = mm_layout_for(LC > 0 ? LC : 1);
+  constexpr MMLayout Lc = mm_layout_for(LC > 0 ? LC : 1, PAC_MM_STAGE != 0);
   const MMLayout& L = LC > 0 ? Lc : Lp;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* lkey = (unsigned long long*)(smem + L.o_lkey);
-  int* lstate = (int*)(smem + L.o_lstate);
   int* lprov = (int*)(smem + L.o_lprov);
   unsigned* lrows = (unsigned*)(smem + L.o_lrows);
   double* bmin = (double*)(smem + L.o_bmin);  // max_j MIN_j, cached (NaN: admit every row)
@@ -476,12 +491,38 @@ __global__ void __launch_bounds__(kThreads, PAC_MM_MINB) k_agg_minmax_v(AggPlan 
   const int64_t t1 = min(ntiles, t0 + t_per);
   const int* kcol = (const int*)p.key_col[0];
   int qh = 0, qn = 0;
+  // staging (PAC_MM_STAGE, ROWS == 4): this thread's 4 keys and 4 values of the next tile
+  constexpr bool STAGE = PAC_MM_STAGE != 0 && ROWS == 4;
+  int4* stk = (int4*)(smem + L.o_stage);
+  double2* stv0 = (double2*)(smem + L.o_stage + kThreads * 16);
+  double2* stv1 = stv0 + kThreads;
+  // dep is 0 at run time but computed from the values just read out of the staging slots, so the
+  // copies that overwrite the slots issue only after those reads completed
+  auto prefetch = [&](int64_t tile, int dep) {
+    const int64_t r0 = tile * T + ROWS * tid;
+    if (tile < t1 && r0 + ROWS <= p.n_rows) {
+      cp_async16(stk + tid, (const int4*)kcol + (r0 >> 2) + dep);
+      cp_async16(stv0 + tid, (const double2*)p.mcol + (r0 >> 1) + dep);
+      cp_async16(stv1 + tid, (const double2*)p.mcol + (r0 >> 1) + 1 + dep);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (STAGE) prefetch(t0, 0);
 #pragma unroll 1
   for (int64_t tile = t0; tile < t1; ++tile) {
     const int64_t r0 = tile * T + ROWS * tid;
     int kq[ROWS];
     double vq[ROWS];
-    if (r0 + ROWS <= p.n_rows) {
+    if (STAGE && r0 + ROWS <= p.n_rows) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      const int4 k4 = stk[tid];
+      const double2 a = stv0[tid], b = stv1[tid];
+      kq[0] = k4.x; kq[1] = k4.y; kq[2] = k4.z; kq[3] = k4.w;
+      vq[0] = a.x; vq[1] = a.y; vq[2] = b.x; vq[3] = b.y;
+      int dep;
+      asm("and.b32 %0, %1, 0;" : "=r"(dep) : "r"(k4.x ^ k4.w ^ __double2loint(a.x) ^ __double2hiint(b.y)));
+      prefetch(tile + 1, dep);
+    } else if (r0 + ROWS <= p.n_rows) {
 #pragma unroll
       for (int g = 0; g < ROWS / 4; ++g) {
         const int4 k4 = __ldcs((const int4*)kcol + (r0 >> 2) + g);
@@ -1287,10 +1328,10 @@ static bool choose_layout(const AccSet& A, int64_t G_cap, int smem_max, int key_
   return true;
 }
 
-static MMLayout mm_layout(int64_t G_cap, int smem_max) {
+static MMLayout mm_layout(int64_t G_cap, int smem_max, bool vstage = false) {
   int Lcap = (int)std::min<int64_t>(std::max<int64_t>(G_cap, 1), 4096);
   for (;;) {
-    const MMLayout L = mm_layout_for(Lcap);
+    const MMLayout L = mm_layout_for(Lcap, vstage);
     if (L.bytes <= smem_max || Lcap == 1) return L;
     Lcap /= 2;
   }
@@ -1642,10 +1683,10 @@ extern "C" int pac_agg_grouped(const int64_t* d_pu_key, const uint64_t* d_mask, 
   bool sorted = false;  // sort-first path: provisional slots already in canonical order
   if (n_rows > 0) {
     if (!A.has_count) {
-      MMLayout L = mm_layout(G_cap, smem_max);
       // one int32 key column, hashed pu keys, 16-byte aligned columns: the vectorized instance
       const bool vec = n_keys == 1 && keys[0].elem_bytes == 4 && d_pu_key && !getenv("PAC_NO_MMV") &&
                        ((uintptr_t)keys[0].d_col & 15) == 0 && ((uintptr_t)A.mcol & 15) == 0;
+      MMLayout L = mm_layout(G_cap, smem_max, vec && PAC_MM_STAGE);
       const int mmk = (A.has_min ? 1 : 0) | (A.has_max ? 2 : 0);
       const bool r8 = false;
       p.ablate = (getenv("PAC_MMV_NOHINT") ? 8 : 0) | (getenv("PAC_MM_HINT_LOG") ? (1 + atoi(getenv("PAC_MM_HINT_LOG"))) << 4 : 0);
