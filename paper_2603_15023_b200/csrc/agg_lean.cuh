@@ -26,6 +26,22 @@ namespace pac {
 #ifndef PAC_LEAN_QBAL
 #define PAC_LEAN_QBAL 0  // (measured slower on C5: 45.8 vs 44.6 ms) owner mode: slot s in TMEM quarter s % 4, its quarter's 4 warps split the slots by runs
 #endif
+#ifndef PAC_LEAN_BTAB
+#define PAC_LEAN_BTAB 1  // 1: mode P's hash draws read their one-hot position from a shared-memory table
+                         // (common.cuh; C2 2.070 -> 2.040 ms; mode O measured 0.7 % slower with it: 44.61 -> 44.90 ms)
+#endif
+#ifndef PAC_LEAN_DYNCOPY
+#define PAC_LEAN_DYNCOPY 1  // 1: owner mode claims the copy-out of the leftovers in 32-row chunks (warps with fewer runs copy more)
+#endif
+#ifndef PAC_LEAN_CLK
+#define PAC_LEAN_CLK 0  // 1 (profiling builds): per-phase clock64 totals of CTA 0's warps, printed at the end
+#endif
+#if PAC_LEAN_CLK
+// the "memory" clobber keeps the clock read on its side of a barrier
+#define LEAN_CLK(i) do { long long c_; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_) :: "memory"); clk[i] += c_ - clk_t; clk_t = c_; } while (0)
+#else
+#define LEAN_CLK(i) do { } while (0)
+#endif
 #ifndef PAC_LEAN_WORKLIST
 #define PAC_LEAN_WORKLIST 0  // 1: owner warps iterate a ballot-built list of their slots with runs
 #endif
@@ -50,7 +66,7 @@ __host__ __device__ constexpr int lean_cc(int ni, int nf) {
 struct LeanLayout {
   int CC, TS;  // carry rows, sorted-buffer rows (T + CC + Lcap)
   int o_mask, o_ival, o_fval, o_cmask, o_cival, o_cfval, o_raw, o_wpv, o_hist, o_cslot, o_dict, o_lprov,
-      o_lrows, o_off, o_tot, o_cpo, o_lfl, o_rdesc, o_queue, o_xcs, o_mbar, o_misc, raw_bytes,
+      o_lrows, o_off, o_tot, o_cpo, o_lfl, o_rdesc, o_queue, o_xcs, o_btab, o_mbar, o_misc, raw_bytes,
       bytes;
 };
 
@@ -81,6 +97,7 @@ __host__ __device__ constexpr LeanLayout lean_layout(int ni, int nf) {
   L.o_rdesc = lay_take(off, (L.TS / 32 + 1) * 4);
   L.o_queue = lay_take(off, kLeanT * 4);
   L.o_xcs = lay_take(off, 32 * 16 + 32 * 8);
+  L.o_btab = lay_take(off, kBtabBytes);  // one-hot pairs of the hash draws (btab_fill)
   L.o_mbar = lay_take(off, 16);
   L.o_misc = lay_take(off, (int)sizeof(Misc));
   L.bytes = off;
@@ -248,6 +265,7 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
   uint4* xcs = (uint4*)(smem + L.o_xcs);
   uint2* xcs2 = (uint2*)(smem + L.o_xcs + 32 * 16);
   unsigned long long* mbar = (unsigned long long*)(smem + L.o_mbar);
+  const uint32_t btab = btab_addr(smem + L.o_btab);
   Misc* misc = (Misc*)(smem + L.o_misc);
   const unsigned long long* rpu = (const unsigned long long*)raw;  // column 0 of the raw tile
 
@@ -274,10 +292,12 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
   }
   if (tid == 0) {
     misc->nlocal = 0;
+    misc->nruns = misc->big = 0;      // per-parity copy-out chunk counters (PAC_LEAN_DYNCOPY)
     misc->pad[0] = misc->pad[1] = 0;  // per-parity "some value needs the generic run body" flags
     mbar_init(mbar, 1);
   }
   if (tid < 32) store_xpose(xcs, xcs2, tid);
+  btab_fill(btab, tid);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -311,6 +331,10 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
   for (int k = 0; k < 4; ++k) cb.cc[k] = cb.co[k] = 0;
   int ncarry = 0;  // rows of the carry area in use (with alignment entries)
 
+#if PAC_LEAN_CLK
+  long long clk[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long clk_t = clock64();
+#endif
   int par = 0;
   for (int64_t t = t0; t < t1; ++t, par ^= 1) {
     const int64_t base = t * T;
@@ -319,7 +343,11 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
     const unsigned char* cs_in = cslot + par * CC;
     unsigned char* cs_out = cslot + (par ^ 1) * CC;
     int* gflag = misc->pad + par;  // bit 0: some |int64| >= 2^26, bit 1: some f64 non-finite
-    if (tid == 0) *gflag = 0;      // its last reader (C of tile t-2) passed two barriers ago
+    int* cpctr = (par ? &misc->big : &misc->nruns);  // copy-out chunk counter of this tile (fields unused here)
+    if (tid == 0) {  // their last readers (C of tile t-2) passed two barriers ago
+      *gflag = 0;
+      *cpctr = 0;
+    }
     if (staged(t)) {
       mbar_wait(mbar, phase);
       phase ^= 1u;
@@ -333,6 +361,7 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
       __syncthreads();
     }
 
+    LEAN_CLK(0);  // wait for the staged tile
     // ---------------- A: slot of every row and its rank within the slot (shared atomic)
     uint32_t sr[RPT];
 #pragma unroll
@@ -352,7 +381,9 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
       }
       sr[j] = r;
     }
+    LEAN_CLK(1);  // A
     __syncthreads();
+    LEAN_CLK(2);  // barrier after A
 
     // ---------------- B, every warp for itself (lane L: slots 4L .. 4L+3): slot totals (carried +
     // new rows), region offsets (even rows: run_body reads 16-byte row pairs), full runs, the
@@ -393,6 +424,7 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
       int ox = (int)(ex & 0xFFFFu), oy = (int)(ex >> 16), oz = zin - sz;
       nruns = owner ? 0 : __shfl_sync(0xffffffffu, zin, 31);
       ncarry_out = min((int)(all >> 16), CC);
+      LEAN_CLK(8);  // B: totals + scans
       LeanB nb;
       uint32_t wv[4];
       int my_oy = 0, my_valid = 0, my_l4 = 0, my_runs = 0;
@@ -461,9 +493,16 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
           const int a = __shfl_up_sync(0xffffffffu, incl, d);
           if (lane >= d) incl += a;
         }
+        if (PAC_LEAN_QBAL == 2) {
+          // round robin over the quarter's slots with work (no scan): the j-th such slot goes to the
+          // quarter's warp j % 4; a slot mostly has one run per tile, so the warps differ by <= 1 run
+          const unsigned wb = __ballot_sync(0xffffffffu, my_work);
+          owned_work = __ballot_sync(0xffffffffu, my_work && (__popc(wb & lt_mask) & 3) == (wid >> 2));
+        } else {
         const int W = max(__shfl_sync(0xffffffffu, incl, 31), 1);
         const int chunk = min(3, (4 * (incl - my_runs) + 2 * my_runs) / W);  // by the run midpoint
         owned_work = __ballot_sync(0xffffffffu, my_work && chunk == (wid >> 2));
+        }
       } else if (PAC_LEAN_WORKLIST) {
         const unsigned wb = __ballot_sync(0xffffffffu, my_work);
 #pragma unroll
@@ -476,6 +515,7 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
     }
     const int ncarry_in = ncarry;
     ncarry = ncarry_out;
+    LEAN_CLK(3);  // B
 
     // ---------------- A2: carried rows into their slot regions (flat); hash word 0 of two new
     // rows at a time, straight to the slot-sorted position
@@ -493,6 +533,7 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
                                   tmax, emax);
         }
       }
+      LEAN_CLK(9);  // A2: copy-in of the carried rows
       unsigned short* wq = qpos + wid * (T / NW);
       unsigned short* wr = qrow + wid * (T / NW);
       int qn = 0;
@@ -504,7 +545,8 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
         const int pa = va ? (int)(wpv[ra >> 16] & 0xFFFFu) + (int)(ra & 0xFFFFu) : 0;
         const int pb = vb ? (int)(wpv[rb >> 16] & 0xFFFFu) + (int)(rb & 0xFFFFu) : 0;
         HashState ha, hb;
-        pac_hash_begin2(rpu[la], rpu[lb], p.salt, ha, hb);
+        if (PAC_LEAN_BTAB && !owner) pac_hash_begin2_bt(rpu[la], rpu[lb], p.salt, ha, hb, btab);
+        else pac_hash_begin2(rpu[la], rpu[lb], p.salt, ha, hb);
         const bool qa = va && ha.k > 0, qb = vb && hb.k > 0;
         if (va) {
           smask[pa] = hash_mask_now(ha);
@@ -564,10 +606,13 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
       // A3: the warp finishes its queued masks from draw word 1 on (R2)
       for (int qi = lane; qi < qn; qi += 32) {
         const int pos = wq[qi];
-        smask[pos] = pac_hash_continue(smask[pos], ((const unsigned long long*)raw)[wr[qi]]);
+        smask[pos] = (PAC_LEAN_BTAB && !owner) ? pac_hash_continue_bt(smask[pos], ((const unsigned long long*)raw)[wr[qi]], btab)
+                                   : pac_hash_continue(smask[pos], ((const unsigned long long*)raw)[wr[qi]]);
       }
     }
+    LEAN_CLK(4);  // A2 + A3
     __syncthreads();
+    LEAN_CLK(5);  // barrier after A2
     if (tid == 0 && staged(t + 1)) issue_tile(p, raw, mbar, base + T, T);  // the raw tile is consumed
 
     // ---------------- C: full 32-row runs into the TMEM table; leftovers to the carry area
@@ -662,7 +707,26 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
           acc.reset();
         }
       }
+      LEAN_CLK(6);  // C: runs
       // leftovers to the carry area (flat over its rows, every warp a share)
+      if (PAC_LEAN_DYNCOPY && owner) {
+        // the runs of a tile are split unevenly (a warp owns ~6 slots, each with a run in ~2 of 3
+        // tiles), and the next barrier waits for the slowest warp: the warps that finish their runs
+        // early take more of the copy-out, 32 carry rows per claim
+        for (;;) {
+          int c = 0;
+          if (lane == 0) c = atomicAdd(cpctr, 32);
+          c = __shfl_sync(0xffffffffu, c, 0);
+          if (c >= ncarry) break;
+          const int i = c + lane;
+          const int s = i < ncarry ? cs_out[i] : 0xFF;
+          if (s != 0xFF) {
+            unsigned long long tm = 0;
+            uint32_t em = 0;
+            lean_copy_row<NI, NF>(cmask, cival, cfval, i, CC, smask, sival, sfval, scpo[s] + i, TS, tm, em);
+          }
+        }
+      } else
       for (int i = tid; i < ncarry; i += kLeanThreads) {
         const int s = cs_out[i];
         if (s == 0xFF) continue;
@@ -671,10 +735,16 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
         lean_copy_row<NI, NF>(cmask, cival, cfval, i, CC, smask, sival, sfval, scpo[s] + i, TS, tm, em);
       }
     }
+    LEAN_CLK(7);  // C: copy-out
     // no barrier: A of the next tile touches only the other parity's counts and the dictionary;
     // B's shared outputs (read by C) are rewritten only after the barrier that follows A
   }
   __syncthreads();  // every leftover is in the carry area
+#if PAC_LEAN_CLK
+  if (blockIdx.x == 0 && lane == 0)
+    printf("LEANCLK w%02d wait %lld A %lld barA %lld Bscan %lld Brest %lld copyin %lld A2 %lld barA2 %lld Cruns %lld Ccopy %lld tiles %lld\n",
+           wid, clk[0], clk[1], clk[2], clk[8], clk[3], clk[9], clk[4], clk[5], clk[6], clk[7], (long long)(t1 - t0));
+#endif
 
   // ---------------- the rows still in the carry area: one partial run per slot (owner / s % 16)
   for (int s = wid; s < Lcap; s += NW) {

@@ -126,6 +126,108 @@ __device__ __forceinline__ void pac_hash_begin2(uint64_t ka, uint64_t kb, uint64
   }
 }
 
+// ---- the same draws with the one-hot position read from a 64-entry shared-memory table
+// (entry p = {p < 32 ? 1 << p : 0, p >= 32 ? 1 << (p - 32) : 0}).  draw_step is 10 alu-pipe
+// instructions of 11 (shifts, selects and logic ops all issue on the half-rate alu pipe), which
+// is what bounds the hash phases.  Here the field becomes a table address with one shift and one
+// LOP3 (the table is 512-byte aligned in the shared window, so base | offset needs no add), the
+// one-hot pair comes through the otherwise idle LSU, the hit test is two logic ops and two
+// compares, and the flip subtracts the one-hot word from each half under the hit predicate (the
+// other half's word is 0; the hit bit is set, so c - b clears it) -- adds ptxas may place on the
+// fma pipe.  Same arithmetic as draw_step (R2), bit for bit.
+constexpr int kBtabBytes = 1024;  // reservation: a 512-byte table at the first 512-aligned address inside
+
+// shared-window address of the table inside the reservation `raw`
+__device__ __forceinline__ uint32_t btab_addr(const void* raw) {
+  return ((uint32_t)__cvta_generic_to_shared(raw) + 511u) & ~511u;
+}
+__device__ __forceinline__ void btab_fill(uint32_t bt, int tid) {
+  if (tid < 64) {
+    const uint32_t lo = tid < 32 ? 1u << tid : 0u, hi = tid >= 32 ? 1u << (tid - 32) : 0u;
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(bt + 8u * tid), "r"(lo), "r"(hi) : "memory");
+  }
+}
+
+__device__ __forceinline__ uint2 btab_load(uint32_t bt, uint64_t w, int t) {
+  const uint32_t wl = (uint32_t)w, wh = (uint32_t)(w >> 32);
+  const int o = 6 * t;  // byte offset of the entry = field * 8
+  uint32_t off;
+  if (o == 0) off = wl << 3;
+  else if (o + 6 <= 32) off = wl >> (o - 3);
+  else if (o >= 32) off = wh >> (o - 35);  // o = 36, 42, 48, 54
+  else off = __funnelshift_r(wl, wh, o - 3);  // o = 30: the field straddles the halves
+  uint2 b;
+  // not volatile: the table is written once before the first barrier, so the loads may move
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(b.x), "=r"(b.y) : "r"((off & 0x1F8u) | bt));
+  return b;
+}
+
+__device__ __forceinline__ void draw_apply(uint2 b, uint32_t& c0, uint32_t& c1, int& k) {
+#if PAC_DRAW_APPLY_C
+  if (((c1 & b.y) | (c0 & b.x)) != 0u && k > 0) {
+    c0 -= b.x;
+    c1 -= b.y;
+    --k;
+  }
+#else
+  asm("{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t"
+      "and.b32 t, %0, %3;\n\t"
+      "setp.gt.s32 q, %2, 0;\n\t"
+      "lop3.and.b32 t|p, %1, %4, t, 0xEA, q;\n\t"  // p = ((c1 & b1) | (c0 & b0)) != 0 && k > 0
+      "@p sub.u32 %0, %0, %3;\n\t"
+      "@p sub.u32 %1, %1, %4;\n\t"
+      "@p add.s32 %2, %2, -1;\n\t}"
+      : "+r"(c0), "+r"(c1), "+r"(k)
+      : "r"(b.x), "r"(b.y));
+#endif
+}
+
+__device__ __forceinline__ void draw_word_bt(uint64_t w, uint64_t& cand, int& k, uint32_t bt) {
+  uint32_t c0 = (uint32_t)cand, c1 = (uint32_t)(cand >> 32);
+#pragma unroll
+  for (int t = 0; t < 10; ++t) draw_apply(btab_load(bt, w, t), c0, c1, k);
+  cand = ((uint64_t)c1 << 32) | c0;
+}
+
+__device__ __forceinline__ uint64_t pac_hash_continue_bt(uint64_t m, uint64_t w, uint32_t bt) {
+  const bool maj = __popcll(m) > 32;
+  uint64_t cand = maj ? m : ~m;
+  int k = maj ? (__popcll(m) - 32) : (32 - __popcll(m));
+#pragma unroll 1
+  for (int word = 1; word < 64 && k > 0; ++word) {
+    w = fmix64(w + kDrawStep);
+    draw_word_bt(w, cand, k, bt);
+  }
+  while (k > 0) {  // safety net of R2 (never reached in practice)
+    const uint64_t low = cand & (~cand + 1ull);
+    cand ^= low;
+    --k;
+  }
+  return maj ? cand : ~cand;
+}
+
+__device__ __forceinline__ void pac_hash_begin2_bt(uint64_t ka, uint64_t kb, uint64_t salt, HashState& a,
+                                                   HashState& b, uint32_t bt) {
+  a.x = fmix64(ka ^ salt);
+  b.x = fmix64(kb ^ salt);
+  const int ca = __popcll(a.x), cb = __popcll(b.x);
+  a.k = (ca > 32) ? (ca - 32) : (32 - ca);
+  b.k = (cb > 32) ? (cb - 32) : (32 - cb);
+  a.cand = (ca > 32) ? a.x : ~a.x;
+  b.cand = (cb > 32) ? b.x : ~b.x;
+  a.w0 = fmix64(a.x ^ kDrawSeed);
+  b.w0 = fmix64(b.x ^ kDrawSeed);
+  uint32_t a0 = (uint32_t)a.cand, a1 = (uint32_t)(a.cand >> 32);
+  uint32_t b0 = (uint32_t)b.cand, b1 = (uint32_t)(b.cand >> 32);
+#pragma unroll
+  for (int t = 0; t < 10; ++t) {
+    draw_apply(btab_load(bt, a.w0, t), a0, a1, a.k);
+    draw_apply(btab_load(bt, b.w0, t), b0, b1, b.k);
+  }
+  a.cand = ((uint64_t)a1 << 32) | a0;
+  b.cand = ((uint64_t)b1 << 32) | b0;
+}
+
 // mask after the draws so far: x with the flipped majority positions toggled
 __device__ __forceinline__ uint64_t hash_mask_now(const HashState& h) {
   return (__popcll(h.x) > 32) ? h.cand : ~h.cand;
