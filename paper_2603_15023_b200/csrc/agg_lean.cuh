@@ -31,7 +31,14 @@ namespace pac {
                          // (common.cuh; C2 2.070 -> 2.040 ms; mode O measured 0.7 % slower with it: 44.61 -> 44.90 ms)
 #endif
 #ifndef PAC_LEAN_DYNCOPY
-#define PAC_LEAN_DYNCOPY 1  // 1: owner mode claims the copy-out of the leftovers in 32-row chunks (warps with fewer runs copy more)
+#define PAC_LEAN_DYNCOPY 1  // 1: owner mode claims the copy-out of the leftovers in chunks (warps with fewer runs copy more)
+#endif
+#ifndef PAC_LEAN_DYNCHUNK
+#define PAC_LEAN_DYNCHUNK 32  // carry rows per claim (a multiple of 32)
+#endif
+#ifndef PAC_LEAN_PREHASH
+#define PAC_LEAN_PREHASH 0  // 1: odd warps hash their first row pair before phase B (B is a serial shuffle chain,
+                            // replicated per warp: half the warps then do throughput-bound work beside it)
 #endif
 #ifndef PAC_LEAN_CLK
 #define PAC_LEAN_CLK 0  // 1 (profiling builds): per-phase clock64 totals of CTA 0's warps, printed at the end
@@ -390,6 +397,12 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
     // leftovers' places in the carry area.  Warp 0 publishes what phase C needs.
     int nruns, ncarry_out;
     unsigned owned_work;  // bit q: owned slot wid + 16 q has runs this tile (mode O)
+    HashState pha, phb;
+    const bool prehash = PAC_LEAN_PREHASH && (wid & 1);
+    if (prehash) {
+      if (PAC_LEAN_BTAB && !owner) pac_hash_begin2_bt(rpu[tid], rpu[tid + kLeanThreads], p.salt, pha, phb, btab);
+      else pac_hash_begin2(rpu[tid], rpu[tid + kLeanThreads], p.salt, pha, phb);
+    }
     {
       const int4 h4 = *(const int4*)(hp + 4 * lane);
       const int n[4] = {h4.x, h4.y, h4.z, h4.w};
@@ -545,7 +558,10 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
         const int pa = va ? (int)(wpv[ra >> 16] & 0xFFFFu) + (int)(ra & 0xFFFFu) : 0;
         const int pb = vb ? (int)(wpv[rb >> 16] & 0xFFFFu) + (int)(rb & 0xFFFFu) : 0;
         HashState ha, hb;
-        if (PAC_LEAN_BTAB && !owner) pac_hash_begin2_bt(rpu[la], rpu[lb], p.salt, ha, hb, btab);
+        if (j == 0 && prehash) {
+          ha = pha;
+          hb = phb;
+        } else if (PAC_LEAN_BTAB && !owner) pac_hash_begin2_bt(rpu[la], rpu[lb], p.salt, ha, hb, btab);
         else pac_hash_begin2(rpu[la], rpu[lb], p.salt, ha, hb);
         const bool qa = va && ha.k > 0, qb = vb && hb.k > 0;
         if (va) {
@@ -715,15 +731,18 @@ __global__ void __launch_bounds__(kLeanThreads, 1) k_agg_lean(AggPlan p, int own
         // early take more of the copy-out, 32 carry rows per claim
         for (;;) {
           int c = 0;
-          if (lane == 0) c = atomicAdd(cpctr, 32);
+          if (lane == 0) c = atomicAdd(cpctr, PAC_LEAN_DYNCHUNK);
           c = __shfl_sync(0xffffffffu, c, 0);
           if (c >= ncarry) break;
-          const int i = c + lane;
-          const int s = i < ncarry ? cs_out[i] : 0xFF;
-          if (s != 0xFF) {
-            unsigned long long tm = 0;
-            uint32_t em = 0;
-            lean_copy_row<NI, NF>(cmask, cival, cfval, i, CC, smask, sival, sfval, scpo[s] + i, TS, tm, em);
+#pragma unroll
+          for (int h = 0; h < PAC_LEAN_DYNCHUNK / 32; ++h) {
+            const int i = c + 32 * h + lane;
+            const int s = i < ncarry ? cs_out[i] : 0xFF;
+            if (s != 0xFF) {
+              unsigned long long tm = 0;
+              uint32_t em = 0;
+              lean_copy_row<NI, NF>(cmask, cival, cfval, i, CC, smask, sival, sfval, scpo[s] + i, TS, tm, em);
+            }
           }
         }
       } else
