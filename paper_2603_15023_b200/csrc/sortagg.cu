@@ -36,6 +36,9 @@ void note_launch();
 void profile_begin(cudaStream_t st, const char* name);
 void profile_end(cudaStream_t st);
 
+#ifndef PAC_SRT_BTAB
+#define PAC_SRT_BTAB 0  // 1: pass 0 hash draws through the shared-memory table of common.cuh (measured slower on C3: 7.27 -> 7.40 ms)
+#endif
 #ifndef PAC_SRT_MINB
 #define PAC_SRT_MINB 3  // resident k_srt_scatter CTAs per SM the register allocation targets
 #endif
@@ -282,6 +285,11 @@ __global__ void __launch_bounds__(kSrtThreads, NV <= 1 ? PAC_SRT_MINB : 2) k_srt
   __shared__ int s_wsum[kSrtW];
   __shared__ int s_tn;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#if PAC_SRT_BTAB
+  __shared__ __align__(16) unsigned char s_bt[P0 ? kBtabBytes : 16];  // one-hot table of the hash draws (common.cuh)
+  const uint32_t bt = btab_addr(s_bt);
+  if (P0) btab_fill(bt, tid);  // the barrier below orders it before the first tile
+#endif
   const unsigned lt = (1u << lane) - 1u;
   const int64_t n = srt_rows(q, b);
   const int64_t ch = srt_chunk(n, gridDim.x);
@@ -344,7 +352,11 @@ __global__ void __launch_bounds__(kSrtThreads, NV <= 1 ? PAC_SRT_MINB : 2) k_srt
 #pragma unroll
       for (int j = 0; j < RPT; j += 2) {
         HashState ha, hb;
+#if PAC_SRT_BTAB
+        pac_hash_begin2_bt(m[j], m[j + 1], q.salt, ha, hb, bt);
+#else
         pac_hash_begin2(m[j], m[j + 1], q.salt, ha, hb);
+#endif
         m[j] = hash_mask_now(ha);
         m[j + 1] = hash_mask_now(hb);
         const bool sa = rk[j] == 0u && ha.k > 0, sb = rk[j + 1] == 0u && hb.k > 0;
@@ -368,7 +380,11 @@ __global__ void __launch_bounds__(kSrtThreads, NV <= 1 ? PAC_SRT_MINB : 2) k_srt
       __syncwarp();
       for (int qi = lane; qi < qn; qi += 32) {
         const int rr = qr[qi];
+#if PAC_SRT_BTAB
+        res[rr] = pac_hash_continue_bt(res[rr], qw[qi], bt);
+#else
         res[rr] = pac_hash_continue(res[rr], qw[qi]);
+#endif
       }
       __syncwarp();
 #pragma unroll
